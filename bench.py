@@ -1,0 +1,329 @@
+"""Benchmark of the hot path.
+
+One *step* = one complete k-point solve (a0 per-k setup, a1-a5 A_r/M
+applies inside a6 CG inside a7 block inverse Lanczos, a8 Rayleigh-Ritz +
+residuals) of BASELINE config 4 (triclinic 128^3, seed-42 noise eps,
+nev = 16) at the next k-point of its 24-point Gamma->(1/2,1/2,1/2) path.
+Ranks take k-points round-robin (weak scaling, no data-path collective).
+
+value  = matvecs/s (all ranks' A_r/M single-vector applications / max-rank
+         device time); kpoints_per_s alongside.
+e2e    = same metric through the C ABI with HOST buffers: eps uploaded
+         (bnf_set_epsilon, host) and lambda read back every step.
+roofline = the dominant kernel: algorithmic bytes / its CUDA-event time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synthetic import configs, eps as E  # noqa: E402
+
+METRIC = "nullspace-free matvecs/s and k-points/s at 128^3 complex128; HBM GB/s vs peak"
+
+# Algorithmic bytes per single-vector application, per pass (n = grid points).
+# Reads + writes of complex128 (16 B) arrays; eps^{-1} is stored as float64.
+PASS_BYTES = {
+    "zfwd": lambda n: 2 * 16 * n + 3 * 16 * n,       # read y1,y2; write 3 components
+    "yfwd": lambda n: 2 * 3 * 16 * n,                 # in place, 3 components
+    "xpass": lambda n: 2 * 3 * 16 * n + 3 * 8 * n,    # in place + eps^{-1}
+    "yadj": lambda n: 2 * 3 * 16 * n,
+    "zadj": lambda n: 3 * 16 * n + 2 * 16 * n,        # read 3 components; write z1,z2
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(idx):
+    cfg = configs.config(idx)
+    return cfg
+
+
+def kappas(cfg, lat):
+    if cfg.kappa_direct is not None:
+        return [lat.kappa_from_raw(k) for k in cfg.kappa_direct]
+    return [lat.kvec_reduce(K) for K in cfg.kpoints]
+
+
+def eps_for(cfg, lat):
+    return E.stacked(E.sample(cfg.shape, cfg.n, lat.a, lat.delta, lat.a_canon))
+
+
+# ----------------------------------------------------------------- oracle arm
+def oracle_rate(cfg, seconds=15.0, max_matvecs=30, min_matvecs=2):
+    """Oracle (numpy, as it stands) matvecs/s on a bounded sample of the
+    same workload: A_r applications at the first k-points."""
+    from oracle import fftop, lattice as olat
+    O = olat.snap(cfg.a_raw, cfg.n)
+    eps = E.sample(cfg.shape, cfg.n, O.a, O.delta, O.a_canon)
+    if cfg.kappa_direct is not None:
+        kap = olat.kappa_from_raw(O, cfg.kappa_direct[1])
+    else:
+        kap = olat.kvec_reduce(O, cfg.kpoints[0])
+    op = fftop.NFSEPOperator(O, kap, eps)
+    y = np.random.default_rng(0).standard_normal(2 * O.nn) + 0j
+    t0 = time.perf_counter()
+    cnt = 0
+    while cnt < max_matvecs and (cnt < min_matvecs or time.perf_counter() - t0 < seconds):
+        y = op.Ar(y)
+        y /= np.linalg.norm(y)
+        cnt += 1
+    dt = time.perf_counter() - t0
+    return cnt / dt, cnt, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = workload(args.config)
+    total = 0
+    tt = 0.0
+    for _ in range(args.warmup):
+        oracle_rate(cfg, seconds=1.0, max_matvecs=2, min_matvecs=1)
+    for _ in range(args.steps):
+        r, c, dt = oracle_rate(cfg, seconds=3.0, max_matvecs=6, min_matvecs=2)
+        total += c
+        tt += dt
+    v = total / tt
+    sample = "%d oracle A_r applications (numpy FFT, 1 thread) at %s, %d steps" % (total, cfg.name, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "matvecs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic", "config": {"workload": cfg.name, "grid": list(cfg.n)},
+        "cpu_baseline": {"value": v, "unit": "matvecs/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours")
+    ap.add_argument("--block", type=int, default=4)
+    ap.add_argument("--guard", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1806_10284_b200 as bnf
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(args.config)
+    lat = bnf.Lattice(cfg.a_raw, cfg.n)
+    eps = eps_for(cfg, lat)
+    ks = kappas(cfg, lat)
+    stream = torch.cuda.Stream()
+    S = bnf.Solver(lat, device=local, stream=stream.cuda_stream, profile=1, block=args.block, guard=args.guard)
+    S.set_epsilon(eps)
+    nev = cfg.nev
+
+    def kidx(step):
+        return (step * world + rank) % len(ks)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    for s in range(args.warmup):
+        S.solve(ks[kidx(s)], nev, allow_noconv=True)
+    S.kernel_times(reset=True)
+    # timed: device-resident inputs
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    mv = 0
+    launches = 0
+    stats = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for s in range(args.steps):
+            lam, st = S.solve(ks[kidx(args.warmup + s)], nev, allow_noconv=True)
+            mv += st["matvecs"]
+            launches += st["kernel_launches"]
+            stats.append(st)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    ktimes = S.kernel_times(reset=True)
+    t_all = torch.tensor([ms, mv, args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t_all.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t_all.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_max = float(tmax[0])
+        mv_tot = float(tsum[1])
+    else:
+        ms_max, mv_tot = ms, float(mv)
+    value = mv_tot / (ms_max / 1000.0)
+    kps = world * args.steps / (ms_max / 1000.0)
+
+    # e2e: host buffers through the C ABI (eps H2D + lambda D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mv2 = 0
+        for s in range(args.steps):
+            S.set_epsilon(eps)                  # host -> device every step
+            lam, st = S.solve(ks[kidx(args.warmup + s)], nev, allow_noconv=True)   # lambda -> host
+            mv2 += st["matvecs"]
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        t2 = torch.tensor([dt, mv2], dtype=torch.float64, device="cuda")
+        if world > 1:
+            m2 = t2.clone()
+            dist.all_reduce(m2, op=dist.ReduceOp.MAX)
+            s2 = t2.clone()
+            dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+            dt, mv2 = float(m2[0]), float(s2[1])
+        e2e = {"value": mv2 / dt, "unit": "matvecs/s", "h2d_bytes_per_step": int(eps.nbytes),
+               "d2h_bytes_per_step": int(8 * nev), "kpoints_per_s": world * args.steps / dt}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    n = lat.nn
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else None
+    roof = None
+    if dom and dom[0] in PASS_BYTES:
+        name, (kms, kcnt) = dom
+        per_vec = PASS_BYTES[name](n)
+        mv_kernel = mv  # every apply launches each pass once per batch
+        total_bytes = per_vec * mv_kernel
+        achieved = total_bytes / (kms / 1000.0) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(name)
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": total_bytes / kcnt,
+                "avg_launch_us": 1000.0 * kms / kcnt, "peak_source": peak_src,
+                "share_of_step": kms / ms}
+    matvec_ms = sum(v[0] for k, v in ktimes.items() if k in PASS_BYTES)
+    matvec_bytes = sum(PASS_BYTES[k](n) for k in PASS_BYTES) * mv
+    cpu = None
+    if not args.no_cpu and world >= 1:
+        r, c, dt = oracle_rate(cfg)
+        cpu = {"value": r, "unit": "matvecs/s", "cores": 1, "kind": "oracle",
+               "sample": "%d oracle A_r applications at %s, k-point 1 (numpy FFT, 1 thread, %.1f s)" % (c, cfg.name, dt)}
+    line = {
+        "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": cfg.name, "grid": list(cfg.n), "nev": nev, "kpoints_on_path": len(ks),
+                   "block": args.block, "guard": args.guard, "tol_outer": 1e-12, "tol_inner": 1e-13,
+                   "l2": "inputs larger than L2 (Krylov basis and work arrays >> 126 MB)",
+                   "parallelism": "k-point replicas x%d" % world},
+        "kpoints_per_s": kps,
+        "matvec_pipeline": {"ms_total": matvec_ms, "algorithmic_GBps": matvec_bytes / (matvec_ms / 1e3) / 1e9
+                            if matvec_ms else None, "share_of_step": matvec_ms / ms},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "solver": {"matvecs_per_kpoint": mv / args.steps,
+                   "outer_steps": [s_["outer_steps"] for s_ in stats],
+                   "converged": all(s_["converged"] for s_ in stats),
+                   "max_residual": max(s_["max_residual"] for s_ in stats)},
+        "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,184 @@
+/*
+ * bnf.h -- C ABI of the B200-native null-space-free Yee-curl band solver.
+ *
+ * Method: Huang, Li, Li, Lin, Lin, Tian, "Eigenvalue problems of discrete
+ * curl operators on various lattices for simulating three dimensional
+ * photonic crystals" (arXiv 1806.10284).  Citations "P:Lnnn" are lines of
+ * that paper's text.
+ *
+ * Problem statement (P:L64-90, L123-226, L323-332, L1642-1646, L2248-2251,
+ * L2396-2398): given primitive lattice vectors, a grid n1 x n2 x n3, the
+ * permittivity sampled at the Yee edge midpoints (B), and a Bloch vector,
+ * find the nev smallest NONZERO eigenvalues lambda = omega^2 (mu0 = eps0 = 1,
+ * lattice units) of  C^* C e = lambda B e,  via the null-space-free
+ * standard problem  A_r y = lambda y,  A_r = Sigma_r Q_r^* B^{-1} Q_r Sigma_r.
+ *
+ * ---------------------------------------------------------------------------
+ * Layouts (all arrays x-fastest, "vec" of P:L331):
+ *   real space   index(a,b,c) = a + n1*(b + n2*c), component l occupies
+ *                [l*n, (l+1)*n);  E_l lives at the Yee point of component l.
+ *   Fourier side index(i,j,k) = i + n1*(j + n2*k);  a 2n vector y = [y1; y2]
+ *                holds the coefficients on the columns Q_1, Q_2 of Q_r
+ *                (P:L2214-2219).  Fourier mode (i,j,k) is the Bloch plane
+ *                wave exp(2 pi i (a g1 + b g2 + c g3)) with
+ *                  g1 = (i + kappa1)/n1,
+ *                  g2 = (j - m1 i/n1 + kappa^2)/n2          (Thm eigK2)
+ *                  g3 = (k - m3 j/n2 + c_b i + kappa^3)/n3  (Thms eigK3)
+ *                i.e. column (i,j,k) of the unitary T of eq. (T);
+ *                the paper's column order (i slowest) is a permutation of ours.
+ *   complex128   interleaved (re, im) doubles.
+ *
+ * Conventions: the caller owns every buffer it passes; the library owns the
+ * opaque handles and their device workspaces.  A handle is not thread-safe.
+ * Device work is issued on opts.stream; every call returns after the stream
+ * has been synchronised.  Every entry point returns a status code; on failure
+ * bnf_last_error() (thread-local) describes it.  There is no CPU fallback:
+ * without a usable CUDA device the solver calls return BNF_ECUDA.
+ */
+#ifndef BNF_H
+#define BNF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNF_VERSION 1
+
+/* status codes */
+#define BNF_OK 0
+#define BNF_EINVAL 1    /* bad argument: grid < 1, NULL pointer, size mismatch, unsupported axis length */
+#define BNF_EGEOM 2     /* P:L143 admissibility violated after canonicalisation, or degenerate snapped cell */
+#define BNF_ENOMEM 3    /* device or host allocation failed */
+#define BNF_ECUDA 4     /* CUDA runtime error (no device, launch failure, ...) */
+#define BNF_ENCCL 5     /* reserved: distributed (slab) mode */
+#define BNF_ENOCONV 6   /* eigensolver did not reach tolerance; partial results + residuals in stats */
+#define BNF_ESTATE 7    /* call order violated (e.g. solve before bnf_set_epsilon) */
+
+/* memory kinds */
+#define BNF_MEM_HOST 0
+#define BNF_MEM_DEVICE 1
+
+/* operators for bnf_apply_Ar */
+#define BNF_OP_AR 0     /* A_r = Sigma_r Q_r^* B^{-1} Q_r Sigma_r   (NFSEP) */
+#define BNF_OP_M 1      /* M   = Q_r^* B^{-1} Q_r                   (CG operator) */
+
+/* vectors for bnf_eigvecs */
+#define BNF_VEC_Y 0     /* NFSEP eigenvectors y (2n complex each, unit 2-norm) */
+#define BNF_VEC_E 1     /* E-field eigenvectors e = B^{-1} Q_r Sigma_r y / sqrt(lambda) (3n complex,
+                           e^* B e = 1), real-space Yee layout, Bloch phase included */
+
+typedef struct bnf_lattice bnf_lattice;
+typedef struct bnf_solver bnf_solver;
+
+/* Snapped lattice (§2.2, eq. transvec).  Matrices column-major:
+   x[3*l + r] is Cartesian component r of vector l. */
+typedef struct {
+    int n[3];            /* grid n1, n2, n3 */
+    int perm[3];         /* canonical vector l is raw vector perm[l] (cyclic relabel, longest first) */
+    int sign3;           /* -1 if canonical a3 was negated to make the triple right-handed */
+    int m[3];            /* m1, m2, m3 */
+    int rho[3];          /* rho1, rho2, rho3: 1 for the obtuse Case II of gamma, beta, alpha */
+    int category;        /* J3 general category 1..4 */
+    double lengths[3];   /* |a1|, |a2|, |a3| (canonical order) */
+    double cos_raw[3];   /* cos gamma', cos beta', cos alpha' before snapping */
+    double cos_snap[3];  /* corrected cos gamma, cos beta, cos alpha */
+    double a[9];         /* corrected vectors a1..a3, eq. (transvec), upper triangular */
+    double a_canon[9];   /* canonical raw vectors in the ORIGINAL Cartesian frame */
+    double l[3];         /* cell extents l1, l2, l3 */
+    double delta[3];     /* grid spacings dx, dy, dz */
+    long long Ag[9];     /* a = diag(delta) Ag: integer lattice in grid units, upper triangular */
+} bnf_lattice_info;
+
+/* Canonicalise and snap.  a_raw: 3 primitive vectors as
+   columns (a_raw[3*l + r]) in any Cartesian frame.  n: grid.  Returns
+   BNF_EINVAL (n < 1), BNF_EGEOM (P:L143 violated, |cos| >= 1 after snapping,
+   m outside [0,n1]x[0,n1]x[0,n2], degenerate cell).  Host-only, no GPU. */
+int bnf_lattice_create(const double a_raw[9], const int n[3], bnf_lattice** out);
+int bnf_lattice_query(const bnf_lattice* lat, bnf_lattice_info* info);
+void bnf_lattice_destroy(bnf_lattice* lat);
+
+/* Reduced Bloch numbers kappa_l = K . a~_l / (2 pi), with K the physical
+   Bloch vector "2 pi k" in the frame of a_raw and a~ the
+   canonical vectors.  Host-only. */
+int bnf_kvec_reduce(const bnf_lattice* lat, const double K_cart[3], double kappa[3]);
+
+typedef struct {
+    int device;                 /* CUDA device ordinal */
+    void* stream;               /* cudaStream_t to issue work on; NULL = legacy default stream */
+    double tol_outer;           /* 1e-12: Ritz relative residual of A_r^{-1} (DESIGN R12) */
+    double tol_inner;           /* 1e-13: CG relative residual ||r|| <= tol ||c|| */
+    int max_outer;              /* max block-Lanczos steps */
+    int max_inner;              /* max CG iterations per solve */
+    int block;                  /* Lanczos block size b >= 1 (DESIGN R13) */
+    int guard;                  /* extra Ritz pairs converged beyond nev */
+    unsigned long long seed;    /* start-block seed (counter-based generator) */
+    int refine;                 /* 1: final subspace-iteration + Rayleigh-Ritz on A_r (DESIGN R15) */
+    int profile;                /* 1: time every kernel with CUDA events (bnf_kernel_times) */
+} bnf_opts;
+
+void bnf_opts_default(bnf_opts* opts);
+
+typedef struct {
+    int outer_steps;            /* block-Lanczos steps */
+    int converged;              /* 1 if all nev + guard Ritz pairs met tol_outer */
+    long long inner_iters;      /* CG iterations summed over right-hand sides */
+    long long matvecs;          /* single-vector applications of M or A_r executed by the kernels */
+    long long kernel_launches;  /* kernels launched during the call */
+    double max_ritz_residual;   /* max_i |beta s_i| / |theta_i| at exit (A_r^{-1} Ritz pairs) */
+    double max_residual;        /* max_i ||A_r y_i - lambda_i y_i|| / ||y_i|| of the returned pairs */
+    double seconds;             /* wall time of the call */
+} bnf_stats;
+
+/* Create a solver for a lattice on opts->device.  Allocates device memory
+   for the operator work arrays.  BNF_EINVAL if an axis length has a prime
+   factor > 31 or exceeds 1024. */
+int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out);
+void bnf_solver_destroy(bnf_solver* s);
+
+/* Permittivity B: eps[3n] = [vec B1; vec B2; vec B3], real-space
+   layout, every value > 0 (BNF_EINVAL otherwise).  mem = BNF_MEM_HOST or
+   BNF_MEM_DEVICE (device pointer to 3n doubles).  Copied; caller keeps ownership. */
+int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem);
+
+/* Per-k setup: reduced Bloch numbers kappa (canonical
+   labelling).  When every kappa_l is an integer (Gamma) the single
+   Fourier mode with g = 0 is masked (Sigma_r = Pi = 0 there; DESIGN R6). */
+int bnf_set_kappa(bnf_solver* s, const double kappa[3]);
+
+/* Hot-path hook: out = op(y) for b vectors.  y, out: DEVICE pointers to
+   complex128 [b][2][n] (Fourier layout).  out may not alias y.  Uses the
+   kappa of the last bnf_set_kappa / bnf_solve. */
+int bnf_apply_Ar(bnf_solver* s, const void* y, void* out, int b, int op);
+
+/* Solve: nev smallest nonzero eigenvalues of the GEP at
+   kappa, ascending, written to lambda[nev] (HOST).  Eigenvectors stay on the
+   device; fetch them with bnf_eigvecs.  stats may be NULL.  Returns
+   BNF_ENOCONV (with results) if the tolerance was not reached. */
+int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf_stats* stats);
+
+/* Eigenvectors of the last solve: kind = BNF_VEC_Y (out: nev x 2n complex)
+   or BNF_VEC_E (out: nev x 3n complex), mem = HOST or DEVICE. */
+int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem);
+
+/* Per-kernel device time (ms) accumulated since the last reset while
+   opts.profile = 1.  Writes up to cap entries: names[i] (static strings),
+   ms[i], launches[i]; returns the number of kernel kinds in *count. */
+int bnf_kernel_times(bnf_solver* s, const char** names, double* ms, long long* launches, int cap, int* count);
+int bnf_kernel_times_reset(bnf_solver* s);
+
+const char* bnf_last_error(void);
+int bnf_version(void);
+
+/* Testing hooks (host-only, no GPU): Hermitian eigensolver used for the
+   Rayleigh-Ritz / block-tridiagonal steps.  a: n x n complex row-major
+   (interleaved), overwritten; w: n eigenvalues ascending; z: n x n complex
+   row-major eigenvectors (columns), may be NULL. */
+int bnf_host_herm_eig(int n, double* a, double* w, double* z);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNF_H */

@@ -1,0 +1,96 @@
+// Device-side parameter blocks and kernel launchers (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bnf {
+
+// One DFT axis: Stockham radix plan + root table e^{2 pi i t / N}.
+struct AxisPlan {
+    int N;
+    int nst;
+    int R[12];
+    const double2* root;
+};
+
+// Per-k mode parameters.  Fourier mode (i,j,k):
+//   g1 = (i + kappa1)/n1
+//   g2 = ((n1 j - m1 i) mod n1n2)/(n1n2) + kh2/n2
+//   g3 = ((n1n2 k - n1 m3 j + cb' i) mod n)/n + kh3/n3
+//   lambda_l = (e^{2 pi i g_l} - 1)/delta_l
+struct ModeP {
+    int n1, n2, n3;
+    long long n, n12;
+    int m1, m3;
+    long long cbp;    // c_b' = m1 m3 - n2 m2 - rho3 n2 m1, reduced into [0, n)
+    long long n1m3;   // n1 m3 reduced into [0, n)
+    double kap1, kh2, kh3;
+    double idelta[3];
+    long long gamma;  // flat index of the masked Gamma mode, or -1
+    double taup;      // fallback threshold for Lambda_p^* Lambda_p (DESIGN R5)
+};
+
+// e^{2 pi i P / n} for integer P in [0, n): lo[P & mask] * hi[P >> shift]
+struct TwP {
+    const double2* lo;
+    const double2* hi;
+    int shift;
+    unsigned long long mask;
+};
+
+struct OpArgs {
+    ModeP mp;
+    TwP tw;
+    AxisPlan px, py, pz;
+    const double* eps_inv;   // [3][n]  1/eps at the Yee points
+    double inv_n;
+    int W_z, W_y, R_x;       // tile widths
+};
+
+struct Profiler;  // host-side, see solver.cu
+
+// launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
+cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st);
+cudaError_t launch_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaStream_t st);
+cudaError_t launch_xpass(const OpArgs& a, double2* U, int nvec, cudaStream_t st);
+cudaError_t launch_zadj(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, cudaStream_t st);
+cudaError_t launch_xfwd_recover(const OpArgs& a, double2* U, int nvec, const double* eps_inv, double scale0,
+                                const double* scales, cudaStream_t st);
+cudaError_t launch_bloch_phase(const OpArgs& a, double2* U, int nvec, double kap1, double kh2, double kh3,
+                               cudaStream_t st);
+
+cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st);
+
+// vectors of length N (complex), nvec of them, stored back to back
+cudaError_t launch_dot_partial(const double2* X, const double2* Y, long long N, int nvec, double2* partial,
+                               int nblk, cudaStream_t st);
+cudaError_t launch_dot_final(const double2* partial, int nblk, int nvec, double2* out, cudaStream_t st);
+cudaError_t launch_gemm_tn_partial(const double2* X, int p, const double2* Y, int q, long long N,
+                                   double2* partial, int nblk, cudaStream_t st);
+cudaError_t launch_gemm_tn_final(const double2* partial, int nblk, int pq, double2* out, cudaStream_t st);
+cudaError_t launch_gemm_nn(const double2* X, int p, const double2* H, int q, double2* Y, long long N,
+                           double alpha, double beta, cudaStream_t st);
+cudaError_t launch_scale_sigma(const double2* X, double2* Y, const double* sigma, long long n, int nvec,
+                               int inverse, cudaStream_t st);
+cudaError_t launch_fill_random(double2* X, long long N, int nvec, unsigned long long seed, long long offset,
+                               const double* sigma, long long n, cudaStream_t st);
+cudaError_t launch_copy(double2* dst, const double2* src, long long count, cudaStream_t st);
+
+// CG (batched over nvec right-hand sides)
+struct CGState {
+    double* rr;       // [nvec] current (r,r)
+    double* rrnew;    // [nvec]
+    double2* pMp;     // [nvec]
+    double* beta;     // [nvec]
+    double* thr;      // [nvec] tol^2 (c,c)
+    int* active;      // [nvec]
+};
+cudaError_t launch_cg_init(const CGState& s, const double2* cdot, int nvec, double tol, cudaStream_t st);
+cudaError_t launch_cg_xr(double2* X, double2* R, const double2* P, const double2* MP, const CGState& s,
+                         long long N, int nvec, double2* partial, int nblk, cudaStream_t st);
+cudaError_t launch_cg_scalars(const CGState& s, const double2* rrnew_c, int nvec, cudaStream_t st);
+cudaError_t launch_cg_p(double2* P, const double2* R, const CGState& s, long long N, int nvec, cudaStream_t st);
+
+}  // namespace bnf

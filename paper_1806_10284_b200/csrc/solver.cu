@@ -1,0 +1,1021 @@
+// Solver handle and the C ABI (include/bnf.h).
+//
+// Hot path per k-point:
+//   a0  per-k setup: kappa-hat, Gamma mask, sigma table            (bnf_set_kappa)
+//   a1-a5 M / A_r apply: 5 fused passes (kernels.cu)               (apply_op)
+//   a6  batched CG on M = Q_r^* B^{-1} Q_r          (cg_solve)
+//   a7  block inverse Lanczos with full reorthogonalisation         (bnf_solve)
+//   a8  Rayleigh-Ritz on A_r, residuals, E-field recovery           (refine / bnf_eigvecs)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "bnf_internal.h"
+#include "kernels.cuh"
+
+struct bnf_lattice {
+    bnf::Lattice L;
+};
+
+namespace bnf {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t _e = (call);                                                                 \
+        if (_e != cudaSuccess) {                                                                 \
+            set_error(std::string("CUDA: ") + cudaGetErrorString(_e) + " at " + #call);          \
+            return BNF_ECUDA;                                                                    \
+        }                                                                                        \
+    } while (0)
+
+// ---------------------------------------------------------------- tables
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+double2 unit_root(long long num, long long den) {  // e^{2 pi i num/den}, exact reduction
+    long long r = num % den;
+    if (r < 0) r += den;
+    long double ang = 2.0L * kPi * (long double)r / (long double)den;
+    return make_double2((double)cosl(ang), (double)sinl(ang));
+}
+
+bool make_plan(int N, std::vector<int>& radices) {
+    radices.clear();
+    if (N < 1 || N > 1024) return false;
+    int m = N;
+    while (m % 8 == 0 && m != 16 && m != 32 && m != 128 && m != 512 && m != 2048) {
+        radices.push_back(8);
+        m /= 8;
+    }
+    while (m % 4 == 0) {
+        radices.push_back(4);
+        m /= 4;
+    }
+    while (m % 2 == 0) {
+        radices.push_back(2);
+        m /= 2;
+    }
+    while (m % 3 == 0) {
+        radices.push_back(3);
+        m /= 3;
+    }
+    for (int p = 5; m > 1 && p <= 31; p += 2) {
+        while (m % p == 0) {
+            radices.push_back(p);
+            m /= p;
+        }
+    }
+    return m == 1 && radices.size() <= 12;
+}
+
+int pow2_floor(int x) {
+    int p = 1;
+    while (p * 2 <= x) p *= 2;
+    return p;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t b) {
+        if (b <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------- profiler
+struct Profiler {
+    bool on = false;
+    long long launches = 0;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<double, long long>> acc;
+    std::vector<std::string> order;
+
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void flush() {
+        for (auto& r : pending) {
+            cudaEventSynchronize(r.b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            auto it = acc.find(r.name);
+            if (it == acc.end()) {
+                acc[r.name] = {0.0, 0};
+                order.push_back(r.name);
+            }
+            acc[r.name].first += ms;
+            acc[r.name].second += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+    ~Profiler() {
+        for (auto& r : pending) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace bnf
+
+using namespace bnf;
+
+struct bnf_solver {
+    Lattice L;
+    bnf_opts o;
+    cudaStream_t st = nullptr;
+    long long n = 0;
+    OpArgs args{};
+    DevBuf root[3], twlo, twhi;
+    DevBuf eps_inv;
+    bool eps_set = false;
+    DevBuf sigma;
+    bool kappa_set = false;
+    double kappa[3] = {0, 0, 0};
+    double kh2 = 0, kh3 = 0;
+    DevBuf U;        // 3n per vector
+    DevBuf cgx, cgr, cgp, cgmp, cgc;   // 2n per vector
+    DevBuf partial;  // reduction partials
+    DevBuf small;    // small device scalars/matrices
+    DevBuf cgstate;
+    CGState cgs{};
+    DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
+    std::vector<double> lam;
+    int nev_last = 0;
+    int* h_flags = nullptr;     // pinned
+    double2* h_small = nullptr;  // pinned scratch for small matrices
+    size_t h_small_cap = 0;
+    int nblk = 592;
+    Profiler prof;
+    long long matvecs = 0;
+    long long inner_iters = 0;
+
+    ~bnf_solver() {
+        if (h_flags) cudaFreeHost(h_flags);
+        if (h_small) cudaFreeHost(h_small);
+    }
+};
+
+namespace {
+
+// Launch wrapper: counts kernels, optionally brackets them with events.
+template <class F>
+int run(bnf_solver* s, const char* name, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (s->prof.on) {
+        a = s->prof.get();
+        b = s->prof.get();
+        cudaEventRecord(a, s->st);
+    }
+    cudaError_t e = f();
+    s->prof.launches++;
+    if (s->prof.on) {
+        cudaEventRecord(b, s->st);
+        s->prof.pending.push_back({name, a, b});
+        if (s->prof.pending.size() > 4096) s->prof.flush();
+    }
+    if (e != cudaSuccess) {
+        set_error(std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+        return BNF_ECUDA;
+    }
+    return BNF_OK;
+}
+
+#define RUN(name, expr)                                              \
+    do {                                                             \
+        int _rc = run(s, name, [&]() -> cudaError_t { return expr; }); \
+        if (_rc != BNF_OK) return _rc;                               \
+    } while (0)
+
+#define TRY(expr)                   \
+    do {                            \
+        int _rc = (expr);           \
+        if (_rc != BNF_OK) return _rc; \
+    } while (0)
+
+int ensure_small_host(bnf_solver* s, size_t count) {
+    if (count <= s->h_small_cap) return BNF_OK;
+    if (s->h_small) cudaFreeHost(s->h_small);
+    s->h_small = nullptr;
+    CK(cudaMallocHost((void**)&s->h_small, count * sizeof(double2)));
+    s->h_small_cap = count;
+    return BNF_OK;
+}
+
+// ------------------------------------------------------------- operator
+int ensure_work(bnf_solver* s, int nvec) {
+    CK(s->U.ensure((size_t)3 * s->n * nvec * sizeof(double2)));
+    return BNF_OK;
+}
+
+// out = op(y) for nvec vectors (device pointers, 2n each)
+int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
+    TRY(ensure_work(s, nvec));
+    double2* U = s->U.as<double2>();
+    RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
+    RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
+    RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
+    RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
+    RUN("zadj", launch_zadj(s->args, U, out, nvec, op, s->st));
+    s->matvecs += nvec;
+    return BNF_OK;
+}
+
+// out[g] (device double2) = X_v^* Y_v, v < nvec, vectors of length N
+int dots(bnf_solver* s, const double2* X, const double2* Y, long long N, int nvec, double2* out) {
+    double2* part = s->partial.as<double2>();
+    RUN("dot", launch_dot_partial(X, Y, N, nvec, part, s->nblk, s->st));
+    RUN("dot_final", launch_dot_final(part, s->nblk, nvec, out, s->st));
+    return BNF_OK;
+}
+
+// H (device, p x q row-major: H[a*q + c]) = X^* Y, q <= 8
+int gemm_tn(bnf_solver* s, const double2* X, int p, const double2* Y, int q, long long N, double2* H) {
+    double2* part = s->partial.as<double2>();
+    const size_t need = (size_t)p * q * s->nblk * sizeof(double2);
+    if (need > s->partial.bytes) CK(s->partial.ensure(need));
+    part = s->partial.as<double2>();
+    RUN("gemm_tn", launch_gemm_tn_partial(X, p, Y, q, N, part, s->nblk, s->st));
+    RUN("gemm_tn_final", launch_gemm_tn_final(part, s->nblk, p * q, H, s->st));
+    return BNF_OK;
+}
+
+// ------------------------------------------------------------------ CG
+// Solve M X = C for nvec right-hand sides: plain CG, no
+// preconditioner, per-column stopping ||r|| <= tol ||c||.
+int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
+    const long long N = 2 * s->n;
+    const size_t vb = (size_t)N * nvec * sizeof(double2);
+    CK(s->cgr.ensure(vb));
+    CK(s->cgp.ensure(vb));
+    CK(s->cgmp.ensure(vb));
+    double2* R = s->cgr.as<double2>();
+    double2* P = s->cgp.as<double2>();
+    double2* MP = s->cgmp.as<double2>();
+    double2* dd = s->small.as<double2>();  // [0..nvec): dots
+    CK(cudaMemsetAsync(X, 0, vb, s->st));
+    RUN("copy", launch_copy(R, C, N * nvec, s->st));
+    RUN("copy", launch_copy(P, C, N * nvec, s->st));
+    TRY(dots(s, R, R, N, nvec, dd));
+    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->o.tol_inner, s->st));
+    int it = 0;
+    for (; it < s->o.max_inner; ++it) {
+        TRY(apply_op(s, P, MP, nvec, BNF_OP_M));
+        TRY(dots(s, P, MP, N, nvec, s->cgs.pMp));
+        RUN("cg_xr", launch_cg_xr(X, R, P, MP, s->cgs, N, nvec, s->partial.as<double2>(), s->nblk, s->st));
+        RUN("dot_final", launch_dot_final(s->partial.as<double2>(), s->nblk, nvec, dd, s->st));
+        RUN("cg_scalars", launch_cg_scalars(s->cgs, dd, nvec, s->st));
+        RUN("cg_p", launch_cg_p(P, R, s->cgs, N, nvec, s->st));
+        CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        if (s->prof.on) s->prof.flush();
+        int act = 0;
+        for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
+        if (act == 0) {
+            ++it;
+            break;
+        }
+    }
+    s->inner_iters += (long long)it * nvec;
+    if (iters_out) *iters_out = it;
+    return BNF_OK;
+}
+
+// Y = Sigma^{-1} CG(M, Sigma^{-1} X)  =  A_r^{-1} X
+int apply_Ar_inv(bnf_solver* s, const double2* X, double2* Y, int nvec) {
+    const long long N = 2 * s->n;
+    CK(s->cgc.ensure((size_t)N * nvec * sizeof(double2)));
+    double2* C = s->cgc.as<double2>();
+    RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->n, nvec, 1, s->st));
+    TRY(cg_solve(s, C, Y, nvec, nullptr));
+    RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->n, nvec, 1, s->st));
+    return BNF_OK;
+}
+
+// Copy a p x q device matrix to host (row-major)
+int get_small(bnf_solver* s, const double2* dev, int count, std::vector<cd>& out) {
+    TRY(ensure_small_host(s, count));
+    CK(cudaMemcpyAsync(s->h_small, dev, count * sizeof(double2), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    out.resize(count);
+    for (int i = 0; i < count; ++i) out[i] = cd(s->h_small[i].x, s->h_small[i].y);
+    return BNF_OK;
+}
+
+int put_small(bnf_solver* s, const std::vector<cd>& in, double2* dev) {
+    TRY(ensure_small_host(s, in.size()));
+    for (size_t i = 0; i < in.size(); ++i) s->h_small[i] = make_double2(in[i].real(), in[i].imag());
+    CK(cudaMemcpyAsync(dev, s->h_small, in.size() * sizeof(double2), cudaMemcpyHostToDevice, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return BNF_OK;
+}
+
+// H = X^* Y for q possibly > 8 (column chunks); host result p x q row-major
+int gram_host(bnf_solver* s, const double2* X, int p, const double2* Y, int q, std::vector<cd>& H) {
+    const long long N = 2 * s->n;
+    H.assign((size_t)p * q, 0.0);
+    double2* Hd = s->small.as<double2>() + 64;
+    std::vector<cd> tmp;
+    for (int c0 = 0; c0 < q; c0 += 8) {
+        const int qc = std::min(8, q - c0);
+        TRY(gemm_tn(s, X, p, Y + (size_t)c0 * N, qc, N, Hd));
+        TRY(get_small(s, Hd, p * qc, tmp));
+        for (int a = 0; a < p; ++a)
+            for (int c = 0; c < qc; ++c) H[(size_t)a * q + c0 + c] = tmp[(size_t)a * qc + c];
+    }
+    return BNF_OK;
+}
+
+// Y[:, c] = beta Y[:, c] + alpha X H[:, c]  (H host p x q row-major; column chunks of 8)
+int gemm_nn_host(bnf_solver* s, const double2* X, int p, const std::vector<cd>& H, int q, double2* Y, double alpha,
+                 double beta) {
+    const long long N = 2 * s->n;
+    double2* Hd = s->small.as<double2>() + 64;
+    for (int c0 = 0; c0 < q; c0 += 8) {
+        const int qc = std::min(8, q - c0);
+        std::vector<cd> sub((size_t)p * qc);
+        for (int a = 0; a < p; ++a)
+            for (int c = 0; c < qc; ++c) sub[(size_t)a * qc + c] = H[(size_t)a * q + c0 + c];
+        TRY(put_small(s, sub, Hd));
+        RUN("gemm_nn", launch_gemm_nn(X, p, Hd, qc, Y + (size_t)c0 * N, N, alpha, beta, s->st));
+    }
+    return BNF_OK;
+}
+
+// Orthonormalise the q columns of W (in place) by Cholesky-QR twice.
+// Returns R (q x q, upper) with W_in = W_out R.  ok=false on rank deficiency.
+int chol_qr2(bnf_solver* s, double2* W, int q, std::vector<cd>& Rtot, bool& ok) {
+    ok = true;
+    Rtot.assign((size_t)q * q, 0.0);
+    for (int i = 0; i < q; ++i) Rtot[(size_t)i * q + i] = 1.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<cd> G, R, Ri;
+        TRY(gram_host(s, W, q, W, q, G));
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < i; ++j) G[(size_t)i * q + j] = std::conj(G[(size_t)j * q + i]);
+        if (!cholesky_upper(q, G, R)) {
+            ok = false;
+            return BNF_OK;
+        }
+        inv_upper(q, R, Ri);
+        if (q <= 8) {
+            TRY(gemm_nn_host(s, W, q, Ri, q, W, 1.0, 0.0));  // in place is safe for one column chunk
+        } else {
+            const long long N = 2 * s->n;
+            CK(s->cgc.ensure((size_t)N * q * sizeof(double2)));
+            TRY(gemm_nn_host(s, W, q, Ri, q, s->cgc.as<double2>(), 1.0, 0.0));
+            RUN("copy", launch_copy(W, s->cgc.as<double2>(), N * q, s->st));
+        }
+        std::vector<cd> Rn((size_t)q * q, 0.0);
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j) {
+                cd acc = 0.0;
+                for (int k = 0; k < q; ++k) acc += R[(size_t)i * q + k] * Rtot[(size_t)k * q + j];
+                Rn[(size_t)i * q + j] = acc;
+            }
+        Rtot.swap(Rn);
+    }
+    return BNF_OK;
+}
+
+int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
+    const Lattice& L = s->L;
+    const int n1 = L.n[0], n2 = L.n[1], n3 = L.n[2];
+    const int m1 = L.m[0], m2 = L.m[1], m3 = L.m[2];
+    const int r1 = L.rho[0], r2 = L.rho[1], r3 = L.rho[2];
+    const double k1 = kappa[0], k2 = kappa[1], k3 = kappa[2];
+    // kappa-hat (Thm eigK2; Thms eigK3 P:L1733/L1872, SURVEY §8 notation)
+    const double kh2 = k2 - ((double)m1 / n1) * k1 + r1 * k1;
+    const double kh3 = k3 - ((double)m2 / n1) * k1 + r2 * k1 - ((double)m3 / n2) * kh2 + r3 * kh2;
+    s->kappa[0] = k1;
+    s->kappa[1] = k2;
+    s->kappa[2] = k3;
+    s->kh2 = kh2;
+    s->kh3 = kh3;
+    ModeP& p = s->args.mp;
+    p.kap1 = k1;
+    p.kh2 = kh2;
+    p.kh3 = kh3;
+    p.gamma = -1;
+    const bool integral = (k1 == std::floor(k1)) && (k2 == std::floor(k2)) && (k3 == std::floor(k3));
+    if (integral) {
+        // Gamma (R6): the mode with g = 0 mod 1, by exact integer arithmetic.
+        const long long K1 = (long long)k1, K2 = (long long)k2, K3 = (long long)k3;
+        const long long n = s->n, n12 = (long long)n1 * n2;
+        long long i0 = ((-K1) % n1 + n1) % n1;
+        const long long t1 = (i0 + K1) / n1;  // exact
+        const long long jnum = (long long)m1 * t1 - K2 - (long long)r1 * K1;
+        long long j0 = ((jnum % n2) + n2) % n2;
+        // g3 numerator: n1n2 k - n1 m3 j + cb' i + n kh3, with n kh3 integral
+        const long long n1kh2 = (long long)n1 * K2 - (long long)m1 * K1 + (long long)r1 * n1 * K1;
+        const long long nkh3 = n * K3 - (long long)n2 * n3 * m2 * K1 + n * r2 * K1 - (long long)n3 * m3 * n1kh2 +
+                               (long long)n2 * n3 * r3 * n1kh2;
+        const long long cb = (long long)m1 * m3 - (long long)n2 * m2 - (long long)r3 * n2 * m1;
+        long long rest = (long long)n1 * m3 * j0 - cb * i0 - nkh3;  // must be n12 * k0 mod n
+        long long k0 = -1;
+        if (rest % n12 == 0) {
+            k0 = ((rest / n12) % n3 + n3) % n3;
+        } else {
+            set_error("internal: Gamma mode not integral");
+            return BNF_EINVAL;
+        }
+        p.gamma = i0 + (long long)n1 * (j0 + (long long)n2 * k0);
+    }
+    RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st));
+    s->kappa_set = true;
+    return BNF_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* bnf_last_error(void) { return g_err.c_str(); }
+int bnf_version(void) { return BNF_VERSION; }
+
+int bnf_lattice_create(const double a_raw[9], const int n[3], bnf_lattice** out) {
+    if (!a_raw || !n || !out) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    auto* l = new (std::nothrow) bnf_lattice;
+    if (!l) return BNF_ENOMEM;
+    int rc = lattice_snap(a_raw, n, l->L);
+    if (rc != BNF_OK) {
+        delete l;
+        return rc;
+    }
+    *out = l;
+    return BNF_OK;
+}
+
+int bnf_lattice_query(const bnf_lattice* lat, bnf_lattice_info* info) {
+    if (!lat || !info) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    const Lattice& L = lat->L;
+    for (int d = 0; d < 3; ++d) {
+        info->n[d] = L.n[d];
+        info->perm[d] = L.perm[d];
+        info->m[d] = L.m[d];
+        info->rho[d] = L.rho[d];
+        info->lengths[d] = L.lengths[d];
+        info->cos_raw[d] = L.cos_raw[d];
+        info->cos_snap[d] = L.cos_snap[d];
+        info->l[d] = L.l[d];
+        info->delta[d] = L.delta[d];
+    }
+    info->sign3 = L.sign3;
+    info->category = j3_category(L);
+    std::memcpy(info->a, L.a, sizeof(L.a));
+    std::memcpy(info->a_canon, L.a_canon, sizeof(L.a_canon));
+    std::memcpy(info->Ag, L.Ag, sizeof(L.Ag));
+    return BNF_OK;
+}
+
+void bnf_lattice_destroy(bnf_lattice* lat) { delete lat; }
+
+int bnf_kvec_reduce(const bnf_lattice* lat, const double K[3], double kappa[3]) {
+    if (!lat || !K || !kappa) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    for (int l = 0; l < 3; ++l) {
+        const double* a = lat->L.a_canon + 3 * l;
+        kappa[l] = (K[0] * a[0] + K[1] * a[1] + K[2] * a[2]) / (2.0 * 3.14159265358979323846);
+    }
+    return BNF_OK;
+}
+
+void bnf_opts_default(bnf_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->device = 0;
+    o->stream = nullptr;
+    o->tol_outer = 1e-12;
+    o->tol_inner = 1e-13;
+    o->max_outer = 60;
+    o->max_inner = 2000;
+    o->block = 4;
+    o->guard = 4;
+    o->seed = 0x5EEDull;
+    o->refine = 1;
+    o->profile = 0;
+}
+
+int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
+    if (!lat || !out) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    bnf_opts o;
+    bnf_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.block < 1 || o.block > 8 || o.guard < 0 || o.max_outer < 1 || o.max_inner < 1) {
+        set_error("invalid solver options (block must be 1..8)");
+        return BNF_EINVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("no CUDA device available (the solver has no CPU fallback)");
+        return BNF_ECUDA;
+    }
+    std::unique_ptr<bnf_solver> s(new (std::nothrow) bnf_solver);
+    if (!s) return BNF_ENOMEM;
+    s->L = lat->L;
+    s->o = o;
+    CK(cudaSetDevice(o.device));
+    s->st = (cudaStream_t)o.stream;
+    s->prof.on = o.profile != 0;
+    const Lattice& L = s->L;
+    const int n1 = L.n[0], n2 = L.n[1], n3 = L.n[2];
+    s->n = (long long)n1 * n2 * n3;
+    const long long n = s->n;
+    // axis plans + root tables
+    AxisPlan* plans[3] = {&s->args.px, &s->args.py, &s->args.pz};
+    for (int d = 0; d < 3; ++d) {
+        std::vector<int> rad;
+        if (!make_plan(L.n[d], rad)) {
+            set_error("axis length " + std::to_string(L.n[d]) + " unsupported (need <= 1024, prime factors <= 31)");
+            return BNF_EINVAL;
+        }
+        AxisPlan& pl = *plans[d];
+        pl.N = L.n[d];
+        pl.nst = (int)rad.size();
+        for (size_t i = 0; i < rad.size(); ++i) pl.R[i] = rad[i];
+        std::vector<double2> h(pl.N);
+        for (int t = 0; t < pl.N; ++t) h[t] = unit_root(t, pl.N);
+        CK(s->root[d].ensure(pl.N * sizeof(double2)));
+        CK(cudaMemcpy(s->root[d].p, h.data(), pl.N * sizeof(double2), cudaMemcpyHostToDevice));
+        pl.root = s->root[d].as<double2>();
+    }
+    // two-level table of e^{2 pi i P / n}
+    int shift = 0;
+    while ((1LL << (2 * shift)) < n) ++shift;
+    const long long nlo = 1LL << shift, nhi = (n + nlo - 1) / nlo;
+    {
+        std::vector<double2> lo(nlo), hi(nhi);
+        for (long long t = 0; t < nlo; ++t) lo[t] = unit_root(t, n);
+        for (long long t = 0; t < nhi; ++t) hi[t] = unit_root(t * nlo, n);
+        CK(s->twlo.ensure(nlo * sizeof(double2)));
+        CK(s->twhi.ensure(nhi * sizeof(double2)));
+        CK(cudaMemcpy(s->twlo.p, lo.data(), nlo * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s->twhi.p, hi.data(), nhi * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    TwP& tw = s->args.tw;
+    tw.lo = s->twlo.as<double2>();
+    tw.hi = s->twhi.as<double2>();
+    tw.shift = shift;
+    tw.mask = (unsigned long long)(nlo - 1);
+    ModeP& p = s->args.mp;
+    p.n1 = n1;
+    p.n2 = n2;
+    p.n3 = n3;
+    p.n = n;
+    p.n12 = (long long)n1 * n2;
+    p.m1 = L.m[0];
+    p.m3 = L.m[2];
+    long long cb = (long long)L.m[0] * L.m[2] - (long long)n2 * L.m[1] - (long long)L.rho[2] * n2 * L.m[0];
+    p.cbp = ((cb % n) + n) % n;
+    p.n1m3 = ((long long)n1 * L.m[2]) % n;
+    for (int d = 0; d < 3; ++d) p.idelta[d] = 1.0 / L.delta[d];
+    p.gamma = -1;
+    p.taup = 1e-6;
+    s->args.inv_n = 1.0 / (double)n;
+    // tile widths: keep each kernel's shared memory <= ~100 KB
+    const int budget = 100 * 1024;
+    s->args.W_z = std::max(1, std::min(16, pow2_floor(budget / (4 * 16 * n3))));
+    s->args.W_y = std::max(1, std::min(16, pow2_floor(budget / (2 * 16 * n2))));
+    int rx = 16;
+    while (rx > 1 && 2 * 16 * n1 * (rx + 1) > budget) rx /= 2;
+    s->args.R_x = std::min(rx, std::max(1, pow2_floor(n2 * 2 - 1)));
+    s->args.W_z = std::min(s->args.W_z, std::max(1, pow2_floor(n1 * 2 - 1)));
+    s->args.W_y = std::min(s->args.W_y, std::max(1, pow2_floor(n1 * 2 - 1)));
+    CK(s->sigma.ensure(n * sizeof(double)));
+    CK(s->eps_inv.ensure(3 * n * sizeof(double)));
+    s->args.eps_inv = s->eps_inv.as<double>();
+    CK(s->partial.ensure((size_t)s->nblk * 64 * sizeof(double2)));
+    CK(s->small.ensure((size_t)(64 + 4096) * sizeof(double2)));
+    CK(s->cgstate.ensure(64 * 6 * sizeof(double) + 64 * sizeof(double2)));
+    {
+        char* b = s->cgstate.as<char>();
+        s->cgs.rr = (double*)b;
+        s->cgs.rrnew = (double*)(b + 64 * 8);
+        s->cgs.beta = (double*)(b + 128 * 8);
+        s->cgs.thr = (double*)(b + 192 * 8);
+        s->cgs.active = (int*)(b + 256 * 8);
+        s->cgs.pMp = (double2*)(b + 384 * 8);
+    }
+    CK(cudaMallocHost((void**)&s->h_flags, 64 * sizeof(int)));
+    *out = s.release();
+    return BNF_OK;
+}
+
+void bnf_solver_destroy(bnf_solver* s) {
+    if (!s) return;
+    cudaStreamSynchronize(s->st);
+    delete s;
+}
+
+int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
+    if (!s || !eps) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    const long long n3 = 3 * s->n;
+    std::vector<double> h(n3);
+    if (mem == BNF_MEM_HOST) {
+        std::memcpy(h.data(), eps, n3 * sizeof(double));
+    } else if (mem == BNF_MEM_DEVICE) {
+        CK(cudaMemcpyAsync(h.data(), eps, n3 * sizeof(double), cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+    } else {
+        set_error("mem must be BNF_MEM_HOST or BNF_MEM_DEVICE");
+        return BNF_EINVAL;
+    }
+    for (long long t = 0; t < n3; ++t) {
+        if (!(h[t] > 0.0) || !std::isfinite(h[t])) {
+            set_error("eps must be finite and > 0");
+            return BNF_EINVAL;
+        }
+        h[t] = 1.0 / h[t];
+    }
+    CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), n3 * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->eps_set = true;
+    return BNF_OK;
+}
+
+int bnf_set_kappa(bnf_solver* s, const double kappa[3]) {
+    if (!s || !kappa) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    TRY(set_kappa_impl(s, kappa));
+    CK(cudaStreamSynchronize(s->st));
+    return BNF_OK;
+}
+
+int bnf_apply_Ar(bnf_solver* s, const void* y, void* out, int b, int op) {
+    if (!s || !y || !out || b < 1 || (op != BNF_OP_AR && op != BNF_OP_M)) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    if (!s->eps_set || !s->kappa_set) {
+        set_error("bnf_set_epsilon and bnf_set_kappa must precede bnf_apply_Ar");
+        return BNF_ESTATE;
+    }
+    TRY(apply_op(s, (const double2*)y, (double2*)out, b, op));
+    CK(cudaStreamSynchronize(s->st));
+    if (s->prof.on) s->prof.flush();
+    return BNF_OK;
+}
+
+int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf_stats* stats) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!s || !kappa || !lambda || nev < 1) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    if (!s->eps_set) {
+        set_error("bnf_set_epsilon must precede bnf_solve");
+        return BNF_ESTATE;
+    }
+    const long long launches0 = s->prof.launches;
+    s->matvecs = 0;
+    s->inner_iters = 0;
+    TRY(set_kappa_impl(s, kappa));
+    const long long N = 2 * s->n;
+    const int b = s->o.block;
+    const int want = nev + s->o.guard;
+    const long long dof = N - (s->args.mp.gamma >= 0 ? 2 : 0);
+    if (want > dof) {
+        set_error("nev + guard exceeds the NFSEP dimension");
+        return BNF_EINVAL;
+    }
+    const int maxsteps = std::max(1, std::min<int>(s->o.max_outer, (int)((dof + b - 1) / b)));
+    const size_t vbytes = (size_t)N * sizeof(double2);
+    CK(s->V.ensure(vbytes * (size_t)b * (maxsteps + 1)));
+    CK(s->Wb.ensure(vbytes * b));
+    CK(s->cgx.ensure(vbytes * b));
+    double2* V = s->V.as<double2>();
+    double2* W = s->Wb.as<double2>();
+    // start block: seeded counter-based normals, Gamma mode masked (R6)
+    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st));
+    bool ok = true;
+    std::vector<cd> R0;
+    TRY(chol_qr2(s, V, b, R0, ok));
+    if (!ok) {
+        set_error("start block rank deficient");
+        return BNF_ENOCONV;
+    }
+    std::vector<std::vector<cd>> As, Bs;  // b x b blocks
+    std::vector<double> theta;
+    std::vector<cd> S;
+    int m = 0;
+    bool converged = false;
+    double maxres = 0.0;
+    for (int step = 0; step < maxsteps; ++step) {
+        double2* Vj = V + (size_t)step * b * N;
+        TRY(apply_Ar_inv(s, Vj, W, b));  // W = A_r^{-1} V_j
+        // full reorthogonalisation, twice (DGKS); accumulate the projections
+        const int p = (step + 1) * b;
+        std::vector<cd> Hacc((size_t)p * b, 0.0), H;
+        for (int pass = 0; pass < 2; ++pass) {
+            TRY(gram_host(s, V, p, W, b, H));
+            TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
+            for (size_t t = 0; t < H.size(); ++t) Hacc[t] += H[t];
+        }
+        std::vector<cd> A((size_t)b * b);
+        for (int i = 0; i < b; ++i)
+            for (int j = 0; j < b; ++j) A[(size_t)i * b + j] = Hacc[(size_t)(step * b + i) * b + j];
+        for (int i = 0; i < b; ++i)  // Hermitian part
+            for (int j = i; j < b; ++j) {
+                cd h = 0.5 * (A[(size_t)i * b + j] + std::conj(A[(size_t)j * b + i]));
+                A[(size_t)i * b + j] = h;
+                A[(size_t)j * b + i] = std::conj(h);
+            }
+        std::vector<cd> Rn;
+        TRY(chol_qr2(s, W, b, Rn, ok));
+        if (!ok) {  // invariant subspace / breakdown: continue with a fresh random block
+            RUN("fill_random", launch_fill_random(W, N, b, s->o.seed + 7919ull * (step + 1), 0,
+                                                  s->sigma.as<double>(), s->n, s->st));
+            for (int pass = 0; pass < 2; ++pass) {
+                TRY(gram_host(s, V, p, W, b, H));
+                TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
+            }
+            TRY(chol_qr2(s, W, b, Rn, ok));
+            if (!ok) {
+                set_error("block Lanczos breakdown");
+                return BNF_ENOCONV;
+            }
+            std::fill(Rn.begin(), Rn.end(), cd(0.0));
+        }
+        As.push_back(A);
+        Bs.push_back(Rn);
+        m = step + 1;
+        RUN("copy", launch_copy(V + (size_t)(step + 1) * b * N, W, N * b, s->st));
+        // block tridiagonal T_m and its eigen-decomposition
+        const int mb = m * b;
+        std::vector<cd> T((size_t)mb * mb, 0.0);
+        for (int k = 0; k < m; ++k) {
+            for (int i = 0; i < b; ++i)
+                for (int j = 0; j < b; ++j) {
+                    T[(size_t)(k * b + i) * mb + k * b + j] = As[k][(size_t)i * b + j];
+                    if (k + 1 < m) {
+                        const cd bij = Bs[k][(size_t)i * b + j];  // B_{k+1}: row block k+1, col block k
+                        T[(size_t)((k + 1) * b + i) * mb + k * b + j] = bij;
+                        T[(size_t)(k * b + j) * mb + (k + 1) * b + i] = std::conj(bij);
+                    }
+                }
+        }
+        std::vector<double> w;
+        std::vector<cd> Z;
+        herm_eig(mb, T, w, &Z);
+        // descending theta (largest theta = smallest lambda)
+        theta.assign(mb, 0.0);
+        S.assign((size_t)mb * mb, 0.0);
+        for (int c = 0; c < mb; ++c) {
+            theta[c] = w[mb - 1 - c];
+            for (int r = 0; r < mb; ++r) S[(size_t)r * mb + c] = Z[(size_t)r * mb + (mb - 1 - c)];
+        }
+        if (mb >= want) {
+            maxres = 0.0;
+            bool all = true;
+            const std::vector<cd>& Bl = Bs.back();
+            for (int c = 0; c < want; ++c) {
+                double r2 = 0.0;
+                for (int i = 0; i < b; ++i) {
+                    cd acc = 0.0;
+                    for (int j = 0; j < b; ++j) acc += Bl[(size_t)i * b + j] * S[(size_t)((m - 1) * b + j) * mb + c];
+                    r2 += std::norm(acc);
+                }
+                const double rel = std::sqrt(r2) / std::fabs(theta[c]);
+                maxres = std::max(maxres, rel);
+                if (!(rel <= s->o.tol_outer)) all = false;
+            }
+            if (all) {
+                converged = true;
+                break;
+            }
+        }
+    }
+    // Ritz vectors Y = V_m S[:, :want]
+    const int mb = m * b;
+    CK(s->Yv.ensure(vbytes * want));
+    double2* Y = s->Yv.as<double2>();
+    {
+        std::vector<cd> Sw((size_t)mb * want);
+        for (int r = 0; r < mb; ++r)
+            for (int c = 0; c < want; ++c) Sw[(size_t)r * want + c] = S[(size_t)r * mb + c];
+        TRY(gemm_nn_host(s, V, mb, Sw, want, Y, 1.0, 0.0));
+    }
+    std::vector<double> lam(want);
+    for (int c = 0; c < want; ++c) lam[c] = 1.0 / theta[c];
+    double maxr_ar = -1.0;
+    if (s->o.refine >= 1) {
+        // Rayleigh-Ritz of A_r on span(Y) (DESIGN R15); optional one step of
+        // subspace (inverse) iteration first.
+        if (s->o.refine >= 2) {
+            for (int c0 = 0; c0 < want; c0 += b) {
+                const int qc = std::min(b, want - c0);
+                TRY(apply_Ar_inv(s, Y + (size_t)c0 * N, s->cgx.as<double2>(), qc));
+                RUN("copy", launch_copy(Y + (size_t)c0 * N, s->cgx.as<double2>(), N * qc, s->st));
+            }
+            std::vector<cd> Rq;
+            TRY(chol_qr2(s, Y, want, Rq, ok));
+        }
+        CK(s->AZ.ensure(vbytes * want));
+        double2* AZ = s->AZ.as<double2>();
+        for (int c0 = 0; c0 < want; c0 += b) {
+            const int qc = std::min(b, want - c0);
+            TRY(apply_op(s, Y + (size_t)c0 * N, AZ + (size_t)c0 * N, qc, BNF_OP_AR));
+        }
+        std::vector<cd> Hm, Zs;
+        TRY(gram_host(s, Y, want, AZ, want, Hm));
+        for (int i = 0; i < want; ++i)
+            for (int j = i; j < want; ++j) {
+                cd h = 0.5 * (Hm[(size_t)i * want + j] + std::conj(Hm[(size_t)j * want + i]));
+                Hm[(size_t)i * want + j] = h;
+                Hm[(size_t)j * want + i] = std::conj(h);
+            }
+        std::vector<double> w;
+        herm_eig(want, Hm, w, &Zs);
+        // rotate: Y <- Y Zs, AZ <- AZ Zs (via the work block in chunks)
+        CK(s->cgc.ensure(vbytes * want));
+        double2* tmp = s->cgc.as<double2>();
+        TRY(gemm_nn_host(s, Y, want, Zs, want, tmp, 1.0, 0.0));
+        RUN("copy", launch_copy(Y, tmp, N * want, s->st));
+        TRY(gemm_nn_host(s, AZ, want, Zs, want, tmp, 1.0, 0.0));
+        RUN("copy", launch_copy(AZ, tmp, N * want, s->st));
+        for (int c = 0; c < want; ++c) lam[c] = w[c];
+        // residuals ||A_r y - lambda y|| (y unit): AZ_c - lambda_c Y_c
+        std::vector<cd> G1, G2, G3;
+        maxr_ar = 0.0;
+        for (int c = 0; c < nev; ++c) {
+            std::vector<cd> ay, yy, aa;
+            TRY(gram_host(s, AZ + (size_t)c * N, 1, AZ + (size_t)c * N, 1, aa));
+            TRY(gram_host(s, Y + (size_t)c * N, 1, AZ + (size_t)c * N, 1, ay));
+            TRY(gram_host(s, Y + (size_t)c * N, 1, Y + (size_t)c * N, 1, yy));
+            const double l = lam[c];
+            const double r2 = aa[0].real() - 2.0 * l * ay[0].real() + l * l * yy[0].real();
+            const double r = std::sqrt(std::fabs(r2)) / std::sqrt(yy[0].real());
+            maxr_ar = std::max(maxr_ar, r);
+        }
+    }
+    s->lam.assign(lam.begin(), lam.begin() + nev);
+    s->nev_last = nev;
+    for (int c = 0; c < nev; ++c) lambda[c] = lam[c];
+    CK(cudaStreamSynchronize(s->st));
+    if (s->prof.on) s->prof.flush();
+    if (stats) {
+        stats->outer_steps = m;
+        stats->converged = converged ? 1 : 0;
+        stats->inner_iters = s->inner_iters;
+        stats->matvecs = s->matvecs;
+        stats->kernel_launches = s->prof.launches - launches0;
+        stats->max_ritz_residual = maxres;
+        stats->max_residual = maxr_ar;
+        stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (!converged) {
+        set_error("block inverse Lanczos did not converge within max_outer steps");
+        return BNF_ENOCONV;
+    }
+    return BNF_OK;
+}
+
+int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
+    if (!s || !out || (kind != BNF_VEC_Y && kind != BNF_VEC_E) || (mem != BNF_MEM_HOST && mem != BNF_MEM_DEVICE)) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    const int nev = s->nev_last;
+    if (nev == 0) {
+        set_error("no eigenvectors: call bnf_solve first");
+        return BNF_ESTATE;
+    }
+    const long long N = 2 * s->n;
+    const cudaMemcpyKind dir = (mem == BNF_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (kind == BNF_VEC_Y) {
+        CK(cudaMemcpyAsync(out, s->Yv.p, (size_t)N * nev * sizeof(double2), dir, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        return BNF_OK;
+    }
+    // e = B^{-1} Q_r Sigma_r y / sqrt(lambda), Bloch phase of eq. (T) included
+    const long long n = s->n;
+    const size_t ebytes = (size_t)3 * n * sizeof(double2);
+    DevBuf scales;
+    CK(scales.ensure(nev * sizeof(double)));
+    std::vector<double> sc(nev);
+    for (int c = 0; c < nev; ++c) sc[c] = 1.0 / std::sqrt(s->lam[c]);
+    CK(cudaMemcpyAsync(scales.p, sc.data(), nev * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    const int chunk = std::max(1, s->o.block);
+    for (int c0 = 0; c0 < nev; c0 += chunk) {
+        const int qc = std::min(chunk, nev - c0);
+        TRY(ensure_work(s, qc));
+        double2* U = s->U.as<double2>();
+        const double2* Yc = s->Yv.as<double2>() + (size_t)c0 * N;
+        RUN("zfwd", launch_zfwd(s->args, Yc, U, qc, BNF_OP_AR, s->st));
+        RUN("yfwd", launch_ypass(s->args, U, qc, 0, s->st));
+        RUN("xfwd_recover", launch_xfwd_recover(s->args, U, qc, s->eps_inv.as<double>(),
+                                                1.0 / std::sqrt((double)n), scales.as<double>() + c0, s->st));
+        RUN("bloch", launch_bloch_phase(s->args, U, qc, s->kappa[0], s->kh2, s->kh3, s->st));
+        CK(cudaMemcpyAsync((char*)out + (size_t)c0 * ebytes, U, ebytes * qc, dir, s->st));
+    }
+    CK(cudaStreamSynchronize(s->st));
+    return BNF_OK;
+}
+
+int bnf_kernel_times(bnf_solver* s, const char** names, double* ms, long long* launches, int cap, int* count) {
+    if (!s || !count) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    s->prof.flush();
+    int k = 0;
+    for (const auto& nm : s->prof.order) {
+        if (k < cap) {
+            auto& e = s->prof.acc[nm];
+            if (names) names[k] = s->prof.acc.find(nm)->first.c_str();
+            if (ms) ms[k] = e.first;
+            if (launches) launches[k] = e.second;
+        }
+        ++k;
+    }
+    *count = k;
+    return BNF_OK;
+}
+
+int bnf_kernel_times_reset(bnf_solver* s) {
+    if (!s) return BNF_EINVAL;
+    s->prof.flush();
+    s->prof.acc.clear();
+    s->prof.order.clear();
+    return BNF_OK;
+}
+
+int bnf_host_herm_eig(int n, double* a, double* w, double* z) {
+    if (n < 0 || (n > 0 && (!a || !w))) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    std::vector<cd> A((size_t)n * n);
+    for (size_t t = 0; t < A.size(); ++t) A[t] = cd(a[2 * t], a[2 * t + 1]);
+    std::vector<double> ww;
+    std::vector<cd> Z;
+    herm_eig(n, A, ww, z ? &Z : nullptr);
+    for (int i = 0; i < n; ++i) w[i] = ww[i];
+    if (z)
+        for (size_t t = 0; t < Z.size(); ++t) {
+            z[2 * t] = Z[t].real();
+            z[2 * t + 1] = Z[t].imag();
+        }
+    return BNF_OK;
+}
+
+}  // extern "C"

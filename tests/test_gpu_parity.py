@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the
+same seeded inputs.
+
+Tolerances: the operator is a chain of 6 complex128
+DFTs (each backward stable, error ~ eps log2 n) and O(1) diagonal factors,
+so the elementwise difference to the oracle's (independent) evaluation is
+bounded by ~1e-14 relative; we test max|gpu - oracle| <= 1e-12 max|oracle|.
+Eigenvalues: 1e-10 relative (BASELINE north_star); eigenvectors:
+||A_r y - lambda y|| / ||y|| <= 1e-8 (north_star), evaluated with the
+oracle's operator.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import curl, fftop, lattice as olat, spectral  # noqa: E402
+from synthetic import configs, eps as E, vectors  # noqa: E402
+
+OP_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def bnf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1806_10284_b200 as m
+    return m
+
+
+def _setup(bnf, a_raw, n, shape, **kw):
+    L = bnf.Lattice(a_raw, n)
+    O = olat.snap(a_raw, n)
+    eps = E.sample(shape, n, O.a, O.delta, O.a_canon)
+    S = bnf.Solver(L, **kw)
+    S.set_epsilon(E.stacked(eps))
+    return L, O, eps, S
+
+
+def _apply_gpu(S, kappa, y, op):
+    S.set_kappa(kappa)
+    b = y.shape[0]
+    yd = torch.from_numpy(np.ascontiguousarray(y)).cuda()
+    od = torch.empty_like(yd)
+    S.apply_Ar(yd, od, b, op)
+    torch.cuda.synchronize()
+    return od.cpu().numpy()
+
+
+SMALL = [
+    ("sc12 config1", configs.sc_vectors(), (12, 12, 12), "sc_sphere", (0.25, 0.15, 0.05)),
+    ("sc Gamma", configs.sc_vectors(), (6, 6, 6), "sc_sphere", (0.0, 0.0, 0.0)),
+    ("sc Gamma shifted", configs.sc_vectors(), (6, 4, 5), "random:1", (1.0, -2.0, 3.0)),
+    ("sc [111] fallback", configs.sc_vectors(), (8, 8, 8), "random:2", (0.1, 0.1, 0.1)),
+    ("fcc X", configs.fcc_vectors(), (8, 8, 8), "fcc_diamond", (0.5, 0.0, 0.5)),
+    ("fcc ragged", configs.fcc_vectors(), (10, 9, 7), "random:3", (0.13, 0.27, 0.41)),
+    ("bcc Gamma cat4", configs.bcc_vectors(), (12, 12, 9), "bcc_sphere_rod", (0.0, 0.0, 0.0)),
+    ("bcc H", configs.bcc_vectors(), (6, 6, 4), "random:4", (0.5, -0.5, 0.5)),
+    ("triclinic", configs.triclinic_vectors(), (10, 6, 12), "random:5", (0.2, -0.3, 0.45)),
+    ("odd primes", configs.triclinic_vectors(1.0, 0.9, 0.8, 70, 100, 110), (7, 5, 11), "random:6",
+     (0.31, 0.07, -0.2)),
+]
+
+
+@pytest.mark.parametrize("name,a,n,shape,kap", SMALL, ids=[c[0] for c in SMALL])
+def test_apply_vs_dense_oracle(bnf, name, a, n, shape, kap):
+    """bnf_apply_Ar vs the oracle's dense A_r (closed-form T, naive O(n^2)
+    DFT) for op = A_r and M, batch b = 3 (several tiles + ragged tails)."""
+    L, O, eps, S = _setup(bnf, a, n, shape)
+    assert L.m == O.m and L.rho == O.rho
+    y = vectors.complex_normal((3, 2 * O.nn), seed=11)
+    for op, opname in ((bnf.OP_AR, "Ar"), (bnf.OP_M, "M")):
+        D = spectral.Ar_dense(O, kap, eps, op=opname)
+        want = y @ D.T
+        got = _apply_gpu(S, kap, y, op)
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err <= OP_TOL, (name, opname, err)
+
+
+def _cfg_case(idx, n=None, kidx=0):
+    cfg = configs.config(idx)
+    n = n or cfg.n
+    O = olat.snap(cfg.a_raw, n)
+    if cfg.kappa_direct is not None:
+        kap = olat.kappa_from_raw(O, cfg.kappa_direct[kidx])
+    else:
+        kap = olat.kvec_reduce(O, cfg.kpoints[kidx])
+    return cfg, n, kap
+
+
+FULL = [(2, None, 3), (3, None, 5), (4, None, 7), (2, (48, 40, 36), 11), (4, (30, 28, 26), 0), (3, (24, 24, 18), 0)]
+
+
+@pytest.mark.parametrize("idx,n,kidx", FULL)
+def test_apply_vs_matrixfree_oracle_full_size(bnf, idx, n, kidx):
+    """Full BASELINE sizes (64^3, 96^3, 128^3) and ragged grids, in the
+    launch configuration bench.py uses: GPU A_r / M vs the oracle's
+    Algorithms-1/2 operator (numpy FFTs), elementwise."""
+    cfg, n, kap = _cfg_case(idx, n, kidx)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    op = fftop.NFSEPOperator(O, kap, eps)
+    y = vectors.complex_normal((1, 2 * O.nn), seed=idx)
+    for code, name in ((bnf.OP_AR, "Ar"), (bnf.OP_M, "M")):
+        want = op.apply(y[0], name)
+        got = _apply_gpu(S, kap, y, code)[0]
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err <= OP_TOL, (n, name, err)
+
+
+def test_apply_256_sampled(bnf):
+    """Config 5 (256^3): M y vs the oracle on a random vector; checked on a
+    sample of 4096 outputs plus the global Hermitian-form invariant
+    y^* M y = sum_l ||T v_l||^2 / eps (real, positive)."""
+    cfg, n, kap = _cfg_case(5)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    op = fftop.NFSEPOperator(O, kap, eps)
+    y = vectors.complex_normal((1, 2 * O.nn), seed=5)
+    want = op.M(y[0])
+    got = _apply_gpu(S, kap, y, bnf.OP_M)[0]
+    idx = np.random.default_rng(0).choice(got.size, 4096, replace=False)
+    err = np.abs(got[idx] - want[idx]).max() / np.abs(want).max()
+    assert err <= OP_TOL
+    q = np.vdot(y[0], got)
+    assert abs(q.imag) <= 1e-12 * abs(q.real) and q.real > 0
+
+
+def test_batch_equals_single(bnf):
+    """Batched application (b = 4) equals four single applications bitwise."""
+    cfg, n, kap = _cfg_case(2, (16, 16, 16), 4)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    y = vectors.complex_normal((4, 2 * O.nn), seed=3)
+    got = _apply_gpu(S, kap, y, bnf.OP_AR)
+    for v in range(4):
+        one = _apply_gpu(S, kap, y[v:v + 1], bnf.OP_AR)[0]
+        assert np.array_equal(one, got[v])
+
+
+def test_unsupported_axis_rejected(bnf):
+    L = bnf.Lattice(configs.sc_vectors(), (37, 8, 8))
+    with pytest.raises(bnf.BnfError) as e:
+        bnf.Solver(L)
+    assert e.value.code == bnf.EINVAL
+
+
+# ------------------------------------------------------------- eigensolver
+def _golden(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+def test_config1_eigenvalues(bnf, golden_dir):
+    """Config 1 (SC 12^3): 10 smallest nonzero GEP eigenvalues equal the
+    oracle's dense plain definition to 1e-10; eigenvector residual
+    ||A_r y - lambda y||/||y|| <= 1e-8 with the oracle's A_r; E-field
+    satisfies the sparse-C GEP C^*C e = lambda B e."""
+    gold = _golden(golden_dir, "config1_dense_oracle.json")
+    cfg = configs.config(1)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, cfg.n, cfg.shape)
+    kap = L.kvec_reduce(cfg.kpoints[0])
+    lam, st = S.solve(kap, 10)
+    np.testing.assert_allclose(lam, gold["lambda"][:10], rtol=1e-10)
+    assert st["converged"] == 1 and st["matvecs"] > 0
+    op = fftop.NFSEPOperator(O, kap, eps)
+    Y = np.zeros((10, 2 * O.nn), dtype=np.complex128)
+    S.eigvecs(bnf.VEC_Y, Y)
+    for i in range(10):
+        r = np.linalg.norm(op.Ar(Y[i]) - lam[i] * Y[i]) / np.linalg.norm(Y[i])
+        assert r <= 1e-8, (i, r)
+    Ef = np.zeros((10, 3 * O.nn), dtype=np.complex128)
+    S.eigvecs(bnf.VEC_E, Ef)
+    C = curl.curl(O, kap)
+    Bd = curl.B_diag(eps)
+    for i in range(10):
+        e = Ef[i]
+        np.testing.assert_allclose(np.vdot(e, Bd * e).real, 1.0, rtol=1e-9)
+        res = np.linalg.norm(C.conj().T @ (C @ e) - lam[i] * Bd * e) / (lam[i] * np.linalg.norm(Bd * e))
+        assert res <= 1e-8, (i, res)
+        # recovery equals the oracle's B^{-1} Q_r Sigma_r y / sqrt(lambda)
+        want = op.recover(Y[i]).ravel() / math.sqrt(lam[i])
+        np.testing.assert_allclose(e, want, atol=1e-11 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("case", range(9))
+def test_small_config_lattices_eigenvalues(bnf, golden_dir, case):
+    """Config lattices/shapes at small grids, k incl. Gamma, vs the
+    oracle's dense NFSEP (tests/golden/small_nfsep_oracle.json)."""
+    c = _golden(golden_dir, "small_nfsep_oracle.json")["cases"][case]
+    cfg = configs.config(c["config"])
+    n = tuple(c["n"])
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    lam, st = S.solve(tuple(c["kappa"]), 8)
+    np.testing.assert_allclose(lam, c["lambda"][:8], rtol=1e-10)
+
+
+def test_degenerate_sc_x_point(bnf):
+    """exact degeneracies at the SC X point are all found."""
+    L, O, eps, S = _setup(bnf, configs.sc_vectors(), (8, 8, 8), "sc_sphere")
+    kap = (0.5, 0.0, 0.0)
+    dense = np.linalg.eigvalsh(spectral.Ar_dense(O, kap, eps))[:10]
+    lam, st = S.solve(kap, 10)
+    np.testing.assert_allclose(lam, dense, rtol=1e-10)
+
+
+def test_vacuum_free_photon(bnf):
+    """eps == 1: eigenvalues are the discrete free-photon closed form."""
+    L, O, eps, S = _setup(bnf, configs.fcc_vectors(), (12, 12, 12), "vacuum:1.0")
+    kap = (0.21, 0.1, -0.3)
+    lam, _ = S.solve(kap, 8)
+    np.testing.assert_allclose(lam, spectral.free_photon(O, kap)[:8], rtol=1e-10)
+
+
+def test_solve_deterministic(bnf):
+    cfg, n, kap = _cfg_case(2, (16, 16, 16), 6)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    l1, s1 = S.solve(kap, 10)
+    l2, s2 = S.solve(kap, 10)
+    assert np.array_equal(l1, l2) and s1["matvecs"] == s2["matvecs"]
