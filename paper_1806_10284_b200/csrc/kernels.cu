@@ -537,39 +537,50 @@ __global__ void __launch_bounds__(256) k_sum_final(const double2* __restrict__ p
 }
 
 // Tall-skinny X^* Y: X has p vectors, Y has q <= Q vectors, length N.
-// partial[(a*q + c)*nblk + blk].  The Y slice stays in registers; X is
-// streamed once.
-template <int Q, int ROWS>
+// Block = 8 warps over a slice of GT_SLICE rows (grid-stride over slices).
+// The Y slice is staged in shared memory; warp w owns the columns a = w mod 8
+// of X, streams X_a over the slice and accumulates into acc[a][c] (owned
+// exclusively by that warp -> deterministic, no atomics).  partial[(a*q+c)*nblk + blk].
+constexpr int GT_SLICE = 512;
+template <int Q>
 __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restrict__ X, int p,
                                                          const double2* __restrict__ Y, int q, long long N,
                                                          double2* __restrict__ partial) {
-    __shared__ double2 red[32];
+    extern __shared__ double2 gsm[];
+    double2* ys = gsm;                       // [Q][GT_SLICE]
+    double2* acc = gsm + Q * GT_SLICE;       // [p][q]
     const int nblk = gridDim.x;
-    const long long row0 = (long long)blockIdx.x * blockDim.x * ROWS + threadIdx.x;
-    double2 yv[ROWS][Q];
-#pragma unroll
-    for (int u = 0; u < ROWS; ++u) {
-        const long long r = row0 + (long long)u * blockDim.x;
-#pragma unroll
-        for (int c = 0; c < Q; ++c) yv[u][c] = (c < q && r < N) ? Y[(size_t)c * N + r] : make_double2(0, 0);
-    }
-    for (int aidx = 0; aidx < p; ++aidx) {
-        double2 xv[ROWS];
-#pragma unroll
-        for (int u = 0; u < ROWS; ++u) {
-            const long long r = row0 + (long long)u * blockDim.x;
-            xv[u] = (r < N) ? X[(size_t)aidx * N + r] : make_double2(0, 0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = threadIdx.x; t < p * q; t += blockDim.x) acc[t] = make_double2(0, 0);
+    for (long long s0 = (long long)blockIdx.x * GT_SLICE; s0 < N; s0 += (long long)gridDim.x * GT_SLICE) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < Q * GT_SLICE; t += blockDim.x) {
+            const int c = t / GT_SLICE, r = t - c * GT_SLICE;
+            ys[t] = (c < q && s0 + r < N) ? Y[(size_t)c * N + s0 + r] : make_double2(0, 0);
         }
+        __syncthreads();
+        for (int aidx = warp; aidx < p; aidx += 8) {
+            const double2* xa = X + (size_t)aidx * N + s0;
+            double2 sum[Q];
 #pragma unroll
-        for (int c = 0; c < Q; ++c) {
-            if (c >= q) break;
-            double2 acc = make_double2(0, 0);
+            for (int c = 0; c < Q; ++c) sum[c] = make_double2(0, 0);
+#pragma unroll 4
+            for (int r = lane; r < GT_SLICE; r += 32) {
+                const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
 #pragma unroll
-            for (int u = 0; u < ROWS; ++u) acc = cadd(acc, cjmul(xv[u], yv[u][c]));
-            acc = block_sum(acc, red);
-            if (threadIdx.x == 0) partial[((size_t)aidx * q + c) * nblk + blockIdx.x] = acc;
+                for (int c = 0; c < Q; ++c) sum[c] = cadd(sum[c], cjmul(x, ys[c * GT_SLICE + r]));
+            }
+#pragma unroll
+            for (int c = 0; c < Q; ++c) {
+                if (c < q) {
+                    const double2 v = warp_sum(sum[c]);
+                    if (lane == 0) acc[aidx * q + c] = cadd(acc[aidx * q + c], v);
+                }
+            }
         }
     }
+    __syncthreads();
+    for (int t = threadIdx.x; t < p * q; t += blockDim.x) partial[(size_t)t * nblk + blockIdx.x] = acc[t];
 }
 
 // Y_c = beta Y_c + alpha sum_a X_a H[a*q + c]   (H on device, p*q <= 4096)
@@ -796,11 +807,17 @@ cudaError_t launch_dot_final(const double2* partial, int nblk, int nvec, double2
 
 cudaError_t launch_gemm_tn_partial(const double2* X, int p, const double2* Y, int q, long long N, double2* partial,
                                    int nblk, cudaStream_t st) {
-    if (q <= 1) k_gemm_tn_partial<1, 4><<<nblk, 256, 0, st>>>(X, p, Y, q, N, partial);
-    else if (q <= 2) k_gemm_tn_partial<2, 4><<<nblk, 256, 0, st>>>(X, p, Y, q, N, partial);
-    else if (q <= 4) k_gemm_tn_partial<4, 4><<<nblk, 256, 0, st>>>(X, p, Y, q, N, partial);
-    else if (q <= 8) k_gemm_tn_partial<8, 2><<<nblk, 256, 0, st>>>(X, p, Y, q, N, partial);
-    else return cudaErrorInvalidValue;
+    const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
+    if (q > 8) return cudaErrorInvalidValue;
+    const size_t sm = ((size_t)Q * GT_SLICE + (size_t)p * q) * sizeof(double2);
+    const void* f = Q == 1 ? (const void*)k_gemm_tn_partial<1> : Q == 2 ? (const void*)k_gemm_tn_partial<2>
+                  : Q == 4 ? (const void*)k_gemm_tn_partial<4> : (const void*)k_gemm_tn_partial<8>;
+    cudaError_t e = set_smem(f, sm);
+    if (e != cudaSuccess) return e;
+    if (Q == 1) k_gemm_tn_partial<1><<<nblk, 256, sm, st>>>(X, p, Y, q, N, partial);
+    else if (Q == 2) k_gemm_tn_partial<2><<<nblk, 256, sm, st>>>(X, p, Y, q, N, partial);
+    else if (Q == 4) k_gemm_tn_partial<4><<<nblk, 256, sm, st>>>(X, p, Y, q, N, partial);
+    else k_gemm_tn_partial<8><<<nblk, 256, sm, st>>>(X, p, Y, q, N, partial);
     return cudaGetLastError();
 }
 

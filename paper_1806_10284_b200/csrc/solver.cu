@@ -448,12 +448,12 @@ int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
         const long long t1 = (i0 + K1) / n1;  // exact
         const long long jnum = (long long)m1 * t1 - K2 - (long long)r1 * K1;
         long long j0 = ((jnum % n2) + n2) % n2;
-        // g3 numerator: n1n2 k - n1 m3 j + cb' i + n kh3, with n kh3 integral
+        // n g3 = n1n2 k - n1 m3 j + cb' i + n1n2 kh3, with n1n2 kh3 integral
         const long long n1kh2 = (long long)n1 * K2 - (long long)m1 * K1 + (long long)r1 * n1 * K1;
-        const long long nkh3 = n * K3 - (long long)n2 * n3 * m2 * K1 + n * r2 * K1 - (long long)n3 * m3 * n1kh2 +
-                               (long long)n2 * n3 * r3 * n1kh2;
+        const long long n12kh3 = n12 * K3 - (long long)n2 * m2 * K1 + n12 * r2 * K1 - (long long)m3 * n1kh2 +
+                                 (long long)n2 * r3 * n1kh2;
         const long long cb = (long long)m1 * m3 - (long long)n2 * m2 - (long long)r3 * n2 * m1;
-        long long rest = (long long)n1 * m3 * j0 - cb * i0 - nkh3;  // must be n12 * k0 mod n
+        long long rest = (long long)n1 * m3 * j0 - cb * i0 - n12kh3;  // must be n12 * k0 mod n
         long long k0 = -1;
         if (rest % n12 == 0) {
             k0 = ((rest / n12) % n3 + n3) % n3;

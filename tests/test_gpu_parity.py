@@ -220,3 +220,24 @@ def test_solve_deterministic(bnf):
     l1, s1 = S.solve(kap, 10)
     l2, s2 = S.solve(kap, 10)
     assert np.array_equal(l1, l2) and s1["matvecs"] == s2["matvecs"]
+
+
+@pytest.mark.parametrize("idx,kidx", [(2, 9), (3, 13), (4, 5)])
+def test_full_size_eigenpairs_residual(bnf, idx, kidx):
+    """Full BASELINE grids: every returned pair satisfies the north-star
+    residual ||A_r y - lambda y|| / ||y|| <= 1e-8 with the ORACLE's A_r, and
+    lambda equals the oracle Rayleigh quotient to 1e-10 (relative)."""
+    cfg, n, kap = _cfg_case(idx, None, kidx)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    lam, st = S.solve(kap, cfg.nev)
+    assert st["converged"] == 1
+    op = fftop.NFSEPOperator(O, kap, eps)
+    Y = np.zeros((cfg.nev, 2 * O.nn), dtype=np.complex128)
+    S.eigvecs(bnf.VEC_Y, Y)
+    for i in range(cfg.nev):
+        Ay = op.Ar(Y[i])
+        nrm = np.linalg.norm(Y[i])
+        r = np.linalg.norm(Ay - lam[i] * Y[i]) / nrm
+        assert r <= 1e-8, (i, r)
+        rq = np.vdot(Y[i], Ay).real / nrm ** 2
+        assert abs(rq - lam[i]) <= 1e-10 * lam[i]
