@@ -35,13 +35,18 @@ from synthetic import configs, eps as E  # noqa: E402
 METRIC = "nullspace-free matvecs/s and k-points/s at 128^3 complex128; HBM GB/s vs peak"
 
 # Algorithmic bytes per single-vector application, per pass (n = grid points).
-# Reads + writes of complex128 (16 B) arrays; eps^{-1} is stored as float64.
+# Reads + writes of complex128 (16 B) arrays; eps^{-1} is read as a uint8 index
+# into a <=256-entry LUT (all BASELINE eps fields have 2 distinct values).
 PASS_BYTES = {
     "zfwd": lambda n: 2 * 16 * n + 3 * 16 * n,       # read y1,y2; write 3 components
     "yfwd": lambda n: 2 * 3 * 16 * n,                 # in place, 3 components
-    "xpass": lambda n: 2 * 3 * 16 * n + 3 * 8 * n,    # in place + eps^{-1}
+    "xpass": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,    # in place + eps^{-1} as uint8 LUT index
     "yadj": lambda n: 2 * 3 * 16 * n,
     "zadj": lambda n: 3 * 16 * n + 2 * 16 * n,        # read 3 components; write z1,z2
+    # CG-fused variants (one CG iteration = zfwd_cg, yfwd, xpass_cg, yadj, zadj_cg)
+    "zfwd_cg": lambda n: 4 * 16 * n + 2 * 16 * n + 3 * 16 * n,   # read r,p; write p; write 3 components
+    "xpass_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    "zadj_cg": lambda n: 3 * 16 * n + 2 * 16 * n + 8 * 16 * n,   # read U, p; read+write x, r
 }
 
 
@@ -170,8 +175,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours")
-    ap.add_argument("--block", type=int, default=4)
-    ap.add_argument("--guard", type=int, default=4)
+    ap.add_argument("--block", type=int, default=2)
+    ap.add_argument("--guard", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -275,11 +280,19 @@ def main():
     peak, peak_src = load_peaks()
     n = lat.nn
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else None
+    # vectors served by the CG-fused passes vs the plain ones (plain y/x passes serve both)
+    mv_cg = mv
+    if "zfwd_cg" in ktimes and "zfwd" in ktimes and ktimes["zfwd"][1] + ktimes["zfwd_cg"][1] > 0:
+        mv_cg = mv * ktimes["zfwd_cg"][1] / (ktimes["zfwd"][1] + ktimes["zfwd_cg"][1])
+    elif "zfwd_cg" not in ktimes:
+        mv_cg = 0
     roof = None
     if dom and dom[0] in PASS_BYTES:
         name, (kms, kcnt) = dom
         per_vec = PASS_BYTES[name](n)
-        mv_kernel = mv  # every apply launches each pass once per batch
+        # every apply launches each pass once per batch: the pass's vector count is
+        # the matvecs it served (fused-CG and plain variants are timed separately)
+        mv_kernel = mv if not name.endswith("_cg") else mv_cg
         total_bytes = per_vec * mv_kernel
         achieved = total_bytes / (kms / 1000.0) / 1e9
         traffic = None
@@ -292,7 +305,8 @@ def main():
                 "avg_launch_us": 1000.0 * kms / kcnt, "peak_source": peak_src,
                 "share_of_step": kms / ms}
     matvec_ms = sum(v[0] for k, v in ktimes.items() if k in PASS_BYTES)
-    matvec_bytes = sum(PASS_BYTES[k](n) for k in PASS_BYTES) * mv
+    matvec_bytes = sum(PASS_BYTES[k](n) * (mv_cg if k.endswith("_cg") else (mv - mv_cg if k.startswith("z") else mv))
+                       for k in ktimes if k in PASS_BYTES)
     cpu = None
     if not args.no_cpu and world >= 1:
         r, c, dt = oracle_rate(cfg)

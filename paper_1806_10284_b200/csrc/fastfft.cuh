@@ -1,0 +1,256 @@
+// Register-resident FFT building blocks for sm_100a (complex128).
+//
+// A length-N DFT along one axis of a tile of W sequences is computed by a
+// group of N2 threads per sequence, each holding N1 = N/N2 elements in
+// registers (N1 % N2 == 0):
+//   stage 1  : N1-point DFT in registers over m        (x[N2 m + t] -> V_t[k1])
+//   twiddle  : V_t[k1] *= w_N^{t k1}
+//   exchange : one shared-memory transpose
+//   stage 2  : N1/N2 N2-point DFTs per thread over t   (-> X[k1 + N1 k2])
+// `fft_fwd` takes the natural ("stage-1") layout and leaves the output in
+// the "stage-2" layout; `fft_mirror` is the same DFT (any sign) run in
+// reverse, from the stage-2 layout back to the natural layout, so a
+// forward/inverse pair needs no extra reordering.  All in-register
+// twiddles are compile-time constants read from __constant__ tables.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace bnf {
+namespace fast {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cjmul(double2 a, double2 b) {  // conj(a) * b
+    return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+template <int S>
+__device__ __forceinline__ double2 mul_i(double2 a) {  // * (S i)
+    return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// ------------------------------------------------ compile-time twiddles
+constexpr double kPiD = 3.14159265358979323846;
+
+__host__ __device__ constexpr double sin_series(double x) {
+    double x2 = x * x, term = x, sum = x;
+    for (int i = 1; i < 14; ++i) {
+        term *= -x2 / ((2.0 * i) * (2.0 * i + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+__host__ __device__ constexpr double cos_series(double x) {
+    double x2 = x * x, term = 1.0, sum = 1.0;
+    for (int i = 1; i < 14; ++i) {
+        term *= -x2 / ((2.0 * i - 1.0) * (2.0 * i));
+        sum += term;
+    }
+    return sum;
+}
+// (cos, sin)(2 pi j / N) with exact integer quadrant/octant reduction
+__host__ __device__ constexpr double trig2pi(long j, long N, bool want_sin) {
+    long r = j % N;
+    if (r < 0) r += N;
+    const long q = (4 * r) / N;          // quadrant
+    const long rr = 4 * r - q * N;       // angle within quadrant = 2 pi rr / (4N)
+    const bool flip = 2 * rr > N;        // use the complement for x > pi/4
+    const double x = 2.0 * kPiD * (double)(flip ? (N - rr) : rr) / (4.0 * (double)N);
+    const double sx = flip ? cos_series(x) : sin_series(x);   // sin of quadrant angle
+    const double cx = flip ? sin_series(x) : cos_series(x);   // cos of quadrant angle
+    double c = 0, s = 0;
+    if (q == 0) { c = cx; s = sx; }
+    else if (q == 1) { c = -sx; s = cx; }
+    else if (q == 2) { c = -cx; s = -sx; }
+    else { c = sx; s = -cx; }
+    return want_sin ? s : c;
+}
+
+template <int N>
+struct TwTab {
+    double c[N];
+    double s[N];
+    constexpr TwTab() : c{}, s{} {
+        for (int j = 0; j < N; ++j) {
+            c[j] = trig2pi(j, N, false);
+            s[j] = trig2pi(j, N, true);
+        }
+    }
+};
+template <int N>
+__constant__ TwTab<N> kTw = TwTab<N>();
+
+template <int N, int S>
+__device__ __forceinline__ double2 ctw(int j) {  // w_N^{S j}, j compile-time after unrolling
+    const int jj = j % N;
+    return make_double2(kTw<N>.c[jj], S > 0 ? kTw<N>.s[jj] : -kTw<N>.s[jj]);
+}
+
+// ------------------------------------------------------- register DFTs
+__host__ __device__ constexpr int first_factor(int n) {
+    return (n % 4 == 0 && n != 8) ? 4 : (n % 2 == 0 ? 2 : (n % 3 == 0 ? 3 : (n % 5 == 0 ? 5 : n)));
+}
+
+template <int N, int S>
+struct DFT {
+    static __device__ __forceinline__ void run(double2* v) {
+        constexpr int A = first_factor(N);
+        constexpr int B = N / A;
+        double2 y[N];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            double2 t[A];
+#pragma unroll
+            for (int a = 0; a < A; ++a) t[a] = v[B * a + b];
+            DFT<A, S>::run(t);
+#pragma unroll
+            for (int k1 = 0; k1 < A; ++k1) y[b * A + k1] = (b * k1 == 0) ? t[k1] : cmul(t[k1], ctw<N, S>(b * k1));
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < A; ++k1) {
+            double2 t[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) t[b] = y[b * A + k1];
+            DFT<B, S>::run(t);
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) v[k1 + A * k2] = t[k2];
+        }
+    }
+};
+
+template <int S>
+struct DFT<1, S> {
+    static __device__ __forceinline__ void run(double2*) {}
+};
+template <int S>
+struct DFT<2, S> {
+    static __device__ __forceinline__ void run(double2* v) {
+        const double2 t = v[0];
+        v[0] = cadd(t, v[1]);
+        v[1] = csub(t, v[1]);
+    }
+};
+template <int S>
+struct DFT<3, S> {
+    static __device__ __forceinline__ void run(double2* v) {
+        const double s3 = 0.86602540378443864676;
+        const double2 t = cadd(v[1], v[2]);
+        const double2 u = cscale(mul_i<S>(csub(v[1], v[2])), s3);
+        const double2 m = csub(v[0], cscale(t, 0.5));
+        v[0] = cadd(v[0], t);
+        v[1] = cadd(m, u);
+        v[2] = csub(m, u);
+    }
+};
+template <int S>
+struct DFT<4, S> {
+    static __device__ __forceinline__ void run(double2* v) {
+        const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+        const double2 b0 = cadd(v[1], v[3]), b1 = mul_i<S>(csub(v[1], v[3]));
+        v[0] = cadd(a0, b0);
+        v[2] = csub(a0, b0);
+        v[1] = cadd(a1, b1);
+        v[3] = csub(a1, b1);
+    }
+};
+template <int S>
+struct DFT<8, S> {
+    static __device__ __forceinline__ void run(double2* v) {
+        double2 e[4] = {v[0], v[2], v[4], v[6]};
+        double2 o[4] = {v[1], v[3], v[5], v[7]};
+        DFT<4, S>::run(e);
+        DFT<4, S>::run(o);
+        const double h = 0.70710678118654752440;
+        const double2 t1 = cscale(cadd(o[1], mul_i<S>(o[1])), h);
+        const double2 t2 = mul_i<S>(o[2]);
+        const double2 t3 = cscale(csub(mul_i<S>(o[3]), o[3]), h);
+        v[0] = cadd(e[0], o[0]);
+        v[4] = csub(e[0], o[0]);
+        v[1] = cadd(e[1], t1);
+        v[5] = csub(e[1], t1);
+        v[2] = cadd(e[2], t2);
+        v[6] = csub(e[2], t2);
+        v[3] = cadd(e[3], t3);
+        v[7] = csub(e[3], t3);
+    }
+};
+
+// ------------------------------------------------ exchange layouts
+// Element (k1, t, w) of a tile.  W-fast: w is the fastest thread index
+// (column tiles of the y/z passes).  T-fast (+1 padding): t fastest (rows of
+// the contiguous x axis).
+template <int N1, int N2, int W>
+struct XchW {
+    static __device__ __forceinline__ int idx(int k1, int t, int w) { return (k1 * N2 + t) * W + w; }
+    static constexpr int size = N1 * N2 * W;
+};
+template <int N1, int N2, int W>
+struct XchT {
+    static __device__ __forceinline__ int idx(int k1, int t, int w) { return (w * N1 + k1) * (N2 + 1) + t; }
+    static constexpr int size = W * N1 * (N2 + 1);
+};
+
+template <int S>
+__device__ __forceinline__ double2 root_tw(const double2* __restrict__ root, int t) {
+    const double2 w = __ldg(root + t);
+    return S > 0 ? w : cconj(w);
+}
+
+// Natural layout -> stage-2 layout.  On exit v[u*N2 + k2] = X[k1 + N1*k2]
+// with k1 = t + N2*u.  Two __syncthreads (buffer free on exit).
+template <int N1, int N2, int S, class X>
+__device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
+    DFT<N1, S>::run(v);
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, t * k1));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) xch[X::idx(k1, t, w)] = v[k1];
+    __syncthreads();
+    constexpr int U = N1 / N2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        double2 a[N2];
+        const int k1 = t + N2 * u;
+#pragma unroll
+        for (int tt = 0; tt < N2; ++tt) a[tt] = xch[X::idx(k1, tt, w)];
+        DFT<N2, S>::run(a);
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) v[u * N2 + k2] = a[k2];
+    }
+    __syncthreads();
+}
+
+// Stage-2 layout -> natural layout (the same DFT run in reverse order).
+template <int N1, int N2, int S, class X>
+__device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
+    constexpr int U = N1 / N2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        double2 a[N2];
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) a[k2] = v[u * N2 + k2];
+        DFT<N2, S>::run(a);
+        const int k1 = t + N2 * u;
+#pragma unroll
+        for (int tt = 0; tt < N2; ++tt) xch[X::idx(k1, tt, w)] = a[tt];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) v[k1] = xch[X::idx(k1, t, w)];
+    __syncthreads();
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, t * k1));
+    }
+    DFT<N1, S>::run(v);
+}
+
+}  // namespace fast
+}  // namespace bnf

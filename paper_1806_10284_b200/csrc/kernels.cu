@@ -18,6 +18,9 @@
 // and are read from an exact two-level table of e^{2 pi i P/n}.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
+#include "fastfft.cuh"
 #include "kernels.cuh"
 
 namespace bnf {
@@ -204,14 +207,15 @@ __device__ __forceinline__ void mode_pis(const ModeP& p, const double2 lam[3], b
         sig = 0.0;
         return;
     }
-    sig = sqrt(q);
+    const double rq = rsqrt(q);
+    sig = q * rq;
     const double2 d1 = csub(lam[2], lam[1]);
     const double2 d2 = csub(lam[0], lam[2]);
     const double2 d3 = csub(lam[1], lam[0]);
     const double p2 = cabs2(d1) + cabs2(d2) + cabs2(d3);
     if (p2 > p.taup * q) {
-        const double r1 = rsqrt(p2 * q);
         const double r2 = rsqrt(p2);
+        const double r1 = r2 * rq;
         pi1[0] = cscale(csub(cjmul(lam[1], d3), cjmul(lam[2], d2)), r1);
         pi1[1] = cscale(csub(cjmul(lam[2], d1), cjmul(lam[0], d3)), r1);
         pi1[2] = cscale(csub(cjmul(lam[0], d2), cjmul(lam[1], d1)), r1);
@@ -222,7 +226,6 @@ __device__ __forceinline__ void mode_pis(const ModeP& p, const double2 lam[3], b
     }
     // R5 fallback: e_m (smallest |lambda_m|, relative tie tolerance -> lowest m)
     // Gram-Schmidt'ed against Pi0, third vector conj(Pi0 x Pi1).
-    const double rq = 1.0 / sig;
     double2 u[3];
     for (int l = 0; l < 3; ++l) u[l] = cscale(lam[l], rq);
     double a[3] = {cabs2(lam[0]), cabs2(lam[1]), cabs2(lam[2])};
@@ -711,6 +714,395 @@ __global__ void k_cg_p(double2* __restrict__ P, const double2* __restrict__ R, C
     }
 }
 
+// ---------------------------------------------- fused-CG reductions
+// Block partial of one double (written by thread 0), then a "last block
+// done" election; the last block reduces all partials in a fixed order
+// (deterministic) and updates the CG scalars.
+__device__ void cg_block_partial(double v, double* slot, double2* scratch) {
+    __syncthreads();   // scratch (shared memory) may still be in use
+    const double2 s = block_sum(make_double2(v, 0.0), scratch);
+    if (threadIdx.x == 0) *slot = s.x;
+}
+__device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2* scratch) {
+    __shared__ int is_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter, 1u);
+        is_last = (prev == total - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last != 0;
+}
+__device__ double block_sum_fixed(const double* part, int nb, double2* scratch) {
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) acc += ((volatile const double*)part)[t];
+    __syncthreads();
+    const double2 s = block_sum(make_double2(acc, 0.0), scratch);
+    __shared__ double res;
+    if (threadIdx.x == 0) res = s.x;
+    __syncthreads();
+    return res;
+}
+__device__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+    for (int v = 0; v < nvec; ++v) {
+        const double pmp = block_sum_fixed(cg.part_x + (size_t)v * nb, nb, scratch);
+        if (threadIdx.x == 0) {
+            cg.pmp[v] = pmp;
+            cg.alpha[v] = (cg.active[v] && pmp > 0.0) ? cg.rr[v] / pmp : 0.0;
+        }
+    }
+    if (threadIdx.x == 0) cg.counter[0] = 0u;
+}
+__device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+    for (int v = 0; v < nvec; ++v) {
+        const double rn = block_sum_fixed(cg.part_z + (size_t)v * nb, nb, scratch);
+        if (threadIdx.x == 0) {
+            const int act = cg.active[v];
+            cg.beta[v] = (act && cg.rr[v] > 0.0) ? rn / cg.rr[v] : 0.0;
+            if (act) cg.rr[v] = rn;
+            cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;
+        }
+    }
+    if (threadIdx.x == 0) cg.counter[1] = 0u;
+}
+
+// ================================================================
+// Fast path: register-resident two-stage FFTs (fastfft.cuh).  Used when an
+// axis length has a plan N = N1 * N2 with N1 % N2 == 0 (all BASELINE grids).
+// ================================================================
+__device__ __forceinline__ unsigned long long yz_base(const ModeP& p, int i, int j) {
+    return (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
+}
+// e^{+2 pi i c N3 / n}
+__device__ __forceinline__ double2 tw_yz_fast(const ModeP& p, const TwP& t, int c, unsigned long long N3) {
+    unsigned long long P;
+    if (p.n <= 16777216LL) P = (unsigned long long)(((unsigned)c * (unsigned)N3) % (unsigned)p.n);
+    else P = ((unsigned long long)c * N3) % (unsigned long long)p.n;
+    return tw_lookup(t, P);
+}
+// e^{-2 pi i b M / n12} with M = m1 i mod n12
+__device__ __forceinline__ double2 tw_xy_fast(const ModeP& p, const TwP& t, int b, unsigned M) {
+    const unsigned r = ((unsigned)b * M) % (unsigned)p.n12;
+    const unsigned P = r == 0 ? 0u : (unsigned)p.n12 - r;
+    return tw_lookup(t, (unsigned long long)P * (unsigned long long)p.n3);
+}
+
+__device__ __forceinline__ unsigned long long mod_add(unsigned long long a, unsigned long long b,
+                                                      unsigned long long n) {
+    a += b;
+    return a >= n ? a - n : a;
+}
+__device__ __forceinline__ unsigned long long mulmod(unsigned long long a, unsigned long long b,
+                                                     unsigned long long n) {
+    return (a * b) % n;   // a, b < n <= 2^30: product < 2^60
+}
+
+// Per-column (i, j) mode constants: lambda1, lambda2 and the integer base of
+// the g3 numerator; lambda3 at row k then needs one sincospi and no division.
+struct ColMode {
+    double2 lam1, lam2;
+    unsigned long long base3;
+    double kh3n3, inv_n;
+};
+__device__ __forceinline__ ColMode col_mode(const ModeP& p, int i, int j) {
+    ColMode cm;
+    double g1 = (i + p.kap1) / p.n1;
+    g1 -= rint(g1);
+    long long num2 = ((long long)p.n1 * j - (long long)p.m1 * i) % p.n12;
+    if (num2 < 0) num2 += p.n12;
+    double g2 = (double)num2 / (double)p.n12 + p.kh2 / p.n2;
+    g2 -= rint(g2);
+    cm.lam1 = cscale(em1(g1), p.idelta[0]);
+    cm.lam2 = cscale(em1(g2), p.idelta[1]);
+    cm.base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
+    cm.kh3n3 = p.kh3 / p.n3;
+    cm.inv_n = 1.0 / (double)p.n;
+    return cm;
+}
+__device__ __forceinline__ double2 col_lam3(const ModeP& p, const ColMode& cm, int k) {
+    unsigned long long num3 = cm.base3 + (unsigned long long)p.n12 * (unsigned long long)k;
+    if (num3 >= (unsigned long long)p.n) num3 -= (unsigned long long)p.n;
+    double g3 = (double)num3 * cm.inv_n + cm.kh3n3;
+    g3 -= rint(g3);
+    return cscale(em1(g3), p.idelta[2]);
+}
+
+// y pass: tile of W columns i, fixed c, FFT over j (length n2 = N1*N2).
+template <int N1, int N2, int W, int ADJ>
+__global__ void __launch_bounds__(W * N2) k_ypass_fast(double2* __restrict__ U, OpArgs a) {
+    extern __shared__ double2 sm[];
+    using X = fast::XchW<N1, N2, W>;
+    const ModeP& p = a.mp;
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const int i = blockIdx.x * W + w, c = blockIdx.y;
+    const bool ok = i < p.n1;
+    double2* col = U + (size_t)(blockIdx.z + a.comp0) * p.n + (size_t)p.n1 * (size_t)p.n2 * c + (ok ? i : 0);
+    // twiddle e^{-+2 pi i b M / n12}, M = m1 i; phase index P(b) = b M mod n12 kept incrementally
+    const unsigned long long n12 = (unsigned long long)p.n12;
+    const unsigned long long M = mulmod((unsigned long long)p.m1, (unsigned long long)(ok ? i : 0), n12);
+    const unsigned long long Pt = mulmod((unsigned long long)t, M, n12);
+    const unsigned long long s3 = (unsigned long long)p.n3;
+    double2 v[N1];
+    {
+        const unsigned long long D = mulmod((unsigned long long)N2, M, n12);
+        unsigned long long P = Pt;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+            const int j = N2 * m + t;
+            double2 x = ok ? col[(size_t)p.n1 * j] : make_double2(0, 0);
+            if (ADJ) x = cmul(x, tw_lookup(a.tw, P * s3));          // conj of e^{-2pi i b M/n12}
+            v[m] = x;
+            P = mod_add(P, D, n12);
+        }
+    }
+    fast::fft_fwd<N1, N2, ADJ ? -1 : 1, X>(v, t, w, sm, a.py.root);
+    if (ok) {
+        const unsigned long long Du = mulmod((unsigned long long)N2, M, n12);
+        const unsigned long long Dk = mulmod((unsigned long long)N1, M, n12);
+        unsigned long long Pu = Pt;
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u) {
+            unsigned long long P = Pu;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int b = t + N2 * u + N1 * k2;
+                double2 x = v[u * N2 + k2];
+                if (!ADJ) x = cmul(x, tw_lookup(a.tw, (P == 0 ? 0ull : n12 - P) * s3));
+                col[(size_t)p.n1 * b] = x;
+                P = mod_add(P, Dk, n12);
+            }
+            Pu = mod_add(Pu, Du, n12);
+        }
+    }
+}
+
+// x pass: R rows (b, c) per block, FFT over a (contiguous), * 1/(n eps), inverse FFT.
+template <int N1, int N2, int R, int CG>
+__global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, OpArgs a, CGFuse cg) {
+    extern __shared__ double2 sm[];
+    using X = fast::XchT<N1, N2, R>;
+    const ModeP& p = a.mp;
+    const int t = threadIdx.x % N2, w = threadIdx.x / N2;
+    const long long rows = (long long)p.n2 * p.n3;
+    const long long r = (long long)blockIdx.x * R + w;
+    const bool ok = r < rows;
+    const int vl = blockIdx.y + a.comp0, l = vl % 3;
+    double2* row = U + (size_t)vl * p.n + (size_t)(ok ? r : 0) * p.n1;
+    const double* er = a.eps_inv + (size_t)l * p.n + (size_t)(ok ? r : 0) * p.n1;
+    const unsigned char* ei = a.eps_idx ? a.eps_idx + (size_t)l * p.n + (size_t)(ok ? r : 0) * p.n1 : nullptr;
+    double2 v[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v[m] = ok ? row[N2 * m + t] : make_double2(0, 0);
+    fast::fft_fwd<N1, N2, 1, X>(v, t, w, sm, a.px.root);
+    double pmp = 0.0;
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            const int aa = t + N2 * u + N1 * k2;
+            const double e_ = a.eps_idx ? __ldg(a.eps_lut + __ldg(ei + aa)) : __ldg(er + aa);
+            const double s_ = ok ? a.inv_n * e_ : 0.0;
+            const double2 x = v[u * N2 + k2];
+            if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);      // (p, M p) = sum |T v|^2 / eps
+            v[u * N2 + k2] = cscale(x, s_);
+        }
+    if (CG) {
+        const int vec = vl / 3;
+        const int nb = gridDim.x * 3;
+        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
+        cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
+        if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm)) cg_finish_alpha(cg, nb, nvec_all, sm);
+    }
+    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root);
+    if (ok) {
+#pragma unroll
+        for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
+    }
+}
+
+// z forward: W columns i, fixed j; Sigma_r/Pi combine (2 -> 3), FFT over k,
+// twiddle.  Threads (l, t, w); shared memory holds the 3 component tiles.
+template <int N1, int N2, int W, int CG>
+__global__ void __launch_bounds__(3 * W * N2) k_zfwd_fast(const double2* __restrict__ Y, double2* __restrict__ U,
+                                                          OpArgs a, int op, double2* __restrict__ Pcg,
+                                                          CGFuse cg) {
+    extern __shared__ double2 sm[];
+    constexpr int N = N1 * N2;
+    constexpr int NT = 3 * W * N2;
+    using X = fast::XchW<N1, N2, W>;
+    const ModeP& p = a.mp;
+    const int tid = threadIdx.x;
+    const int w = tid % W, t = (tid / W) % N2, l = tid / (W * N2);
+    const int i = blockIdx.x * W + w, j = blockIdx.y, vec = blockIdx.z;
+    const bool ok = i < p.n1;
+    const long long n = p.n;
+    const size_t colofs = (size_t)(ok ? i : 0) + (size_t)p.n1 * j;
+    const size_t kstride = (size_t)p.n1 * p.n2;
+    // phase 1: every element once; thread keeps column w (NT is a multiple of W).
+    // All loads are issued before the mode algebra (memory-level parallelism).
+    {
+        constexpr int S = (N * W + NT - 1) / NT;
+        const double2* y1 = Y + (size_t)vec * 2 * n + colofs;
+        const double2* y2 = y1 + n;
+        double2 a1[S], a2[S];
+#pragma unroll
+        for (int s_ = 0; s_ < S; ++s_) {
+            const int e = tid + s_ * NT;
+            const bool in = ok && e < N * W;
+            const int k = e / W;
+            a1[s_] = in ? y1[kstride * k] : make_double2(0, 0);
+            a2[s_] = in ? y2[kstride * k] : make_double2(0, 0);
+        }
+        if (CG) {   // p <- r + beta p  (CG direction update fused into the operator's first pass)
+            const double beta = cg.beta[vec];
+            double2* p1 = Pcg + (size_t)vec * 2 * n + colofs;
+            double2* p2 = p1 + n;
+#pragma unroll
+            for (int s_ = 0; s_ < S; ++s_) {
+                const int e = tid + s_ * NT;
+                if (ok && e < N * W) {
+                    const int k = e / W;
+                    const double2 q1 = p1[kstride * k], q2 = p2[kstride * k];
+                    a1[s_] = make_double2(a1[s_].x + beta * q1.x, a1[s_].y + beta * q1.y);
+                    a2[s_] = make_double2(a2[s_].x + beta * q2.x, a2[s_].y + beta * q2.y);
+                    p1[kstride * k] = a1[s_];
+                    p2[kstride * k] = a2[s_];
+                }
+            }
+        }
+        const ColMode cm = col_mode(p, i, j);
+#pragma unroll
+        for (int s_ = 0; s_ < S; ++s_) {
+            const int e = tid + s_ * NT;
+            if (e < N * W) {
+                const int k = e / W;
+                double2 lam[3], pi1[3], pi2[3];
+                double sig;
+                lam[0] = cm.lam1;
+                lam[1] = cm.lam2;
+                lam[2] = col_lam3(p, cm, k);
+                mode_pis(p, lam, (long long)(colofs + kstride * k) == p.gamma, pi1, pi2, sig);
+                const double sc = (op == 0) ? sig : 1.0;
+#pragma unroll
+                for (int ll = 0; ll < 3; ++ll)
+                    sm[ll * N * W + e] = cscale(cadd(cmul(pi1[ll], a1[s_]), cmul(pi2[ll], a2[s_])), sc);
+            }
+        }
+    }
+    __syncthreads();
+    double2* tile = sm + (size_t)l * N * W;
+    double2 v[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v[m] = tile[(N2 * m + t) * W + w];
+    __syncthreads();
+    fast::fft_fwd<N1, N2, 1, X>(v, t, w, tile, a.pz.root);
+    if (ok) {
+        const unsigned long long nn = (unsigned long long)n;
+        const unsigned long long N3 = yz_base(p, i, j);
+        const unsigned long long Du = mulmod((unsigned long long)N2, N3, nn);
+        const unsigned long long Dk = mulmod((unsigned long long)N1, N3, nn);
+        unsigned long long Pu = mulmod((unsigned long long)t, N3, nn);
+        double2* out = U + (size_t)vec * 3 * n + (size_t)l * n + colofs;
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u) {
+            unsigned long long P = Pu;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int c = t + N2 * u + N1 * k2;
+                out[kstride * c] = cmul(v[u * N2 + k2], tw_lookup(a.tw, P));
+                P = mod_add(P, Dk, nn);
+            }
+            Pu = mod_add(Pu, Du, nn);
+        }
+    }
+}
+
+// z adjoint: conj twiddle, FFT (-) over c, then Pi^* combine (3 -> 2), Sigma_r.
+template <int N1, int N2, int W, int CG>
+__global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restrict__ U, double2* __restrict__ OUT,
+                                                          OpArgs a, int op, CGFuse cg) {
+    extern __shared__ double2 sm[];
+    constexpr int N = N1 * N2;
+    constexpr int NT = 3 * W * N2;
+    using X = fast::XchW<N1, N2, W>;
+    const ModeP& p = a.mp;
+    const int tid = threadIdx.x;
+    const int w = tid % W, t = (tid / W) % N2, l = tid / (W * N2);
+    const int i = blockIdx.x * W + w, j = blockIdx.y, vec = blockIdx.z;
+    const bool ok = i < p.n1;
+    const long long n = p.n;
+    const size_t colofs = (size_t)(ok ? i : 0) + (size_t)p.n1 * j;
+    const size_t kstride = (size_t)p.n1 * p.n2;
+    double2* tile = sm + (size_t)l * N * W;
+    double2 v[N1];
+    {
+        const unsigned long long nn = (unsigned long long)n;
+        const unsigned long long N3 = yz_base(p, i, j);
+        const unsigned long long D = mulmod((unsigned long long)N2, N3, nn);
+        unsigned long long P = mulmod((unsigned long long)t, N3, nn);
+        const double2* in = U + (size_t)vec * 3 * n + (size_t)l * n + colofs;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+            const int c = N2 * m + t;
+            v[m] = ok ? cmul(in[kstride * c], tw_lookup(a.tw, P == 0 ? 0ull : nn - P)) : make_double2(0, 0);
+            P = mod_add(P, D, nn);
+        }
+    }
+    fast::fft_fwd<N1, N2, -1, X>(v, t, w, tile, a.pz.root);
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) tile[(t + N2 * u + N1 * k2) * W + w] = v[u * N2 + k2];
+    __syncthreads();
+    double rr = 0.0;
+    if (ok) {
+        double2* o1 = OUT + (size_t)vec * 2 * n + colofs;
+        double2* o2 = o1 + n;
+        const ColMode cm = col_mode(p, i, j);
+        const double alpha = CG ? cg.alpha[vec] : 0.0;
+        for (int e = tid; e < N * W; e += NT) {
+            const int k = e / W;
+            double2 lam[3], pi1[3], pi2[3];
+            double sig;
+            lam[0] = cm.lam1;
+            lam[1] = cm.lam2;
+            lam[2] = col_lam3(p, cm, k);
+            mode_pis(p, lam, (long long)(colofs + kstride * k) == p.gamma, pi1, pi2, sig);
+            const double2 w0 = sm[e], w1 = sm[N * W + e], w2 = sm[2 * N * W + e];
+            double2 z1 = cadd(cadd(cjmul(pi1[0], w0), cjmul(pi1[1], w1)), cjmul(pi1[2], w2));
+            double2 z2 = cadd(cadd(cjmul(pi2[0], w0), cjmul(pi2[1], w1)), cjmul(pi2[2], w2));
+            const double sc = (op == 0) ? sig : 1.0;
+            z1 = cscale(z1, sc);
+            z2 = cscale(z2, sc);
+            if (CG) {   // OUT = x (solution), cg.X2 = r (residual), cg.P = p
+                const size_t o = kstride * k;
+                const size_t base = (size_t)vec * 2 * n + colofs;
+                const double2 pp1 = cg.P[base + o], pp2 = cg.P[base + n + o];
+                double2 r1 = cg.R[base + o], r2 = cg.R[base + n + o];
+                double2 x1 = o1[o], x2 = o2[o];
+                x1 = make_double2(x1.x + alpha * pp1.x, x1.y + alpha * pp1.y);
+                x2 = make_double2(x2.x + alpha * pp2.x, x2.y + alpha * pp2.y);
+                r1 = make_double2(r1.x - alpha * z1.x, r1.y - alpha * z1.y);
+                r2 = make_double2(r2.x - alpha * z2.x, r2.y - alpha * z2.y);
+                o1[o] = x1;
+                o2[o] = x2;
+                cg.R[base + o] = r1;
+                cg.R[base + n + o] = r2;
+                rr += r1.x * r1.x + r1.y * r1.y + r2.x * r2.x + r2.y * r2.y;
+            } else {
+                o1[kstride * k] = z1;
+                o2[kstride * k] = z2;
+            }
+        }
+    }
+    if (CG) {
+        const int nb = gridDim.x * gridDim.y;
+        cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, sm);
+        if (cg_last_block(cg.counter + 1, gridDim.x * gridDim.y * gridDim.z, sm)) cg_finish_beta(cg, nb, gridDim.z, sm);
+    }
+}
+
 inline int grid_for(long long total, int threads, int cap = 148 * 16) {
     long long g = (total + threads - 1) / threads;
     if (g < 1) g = 1;
@@ -718,6 +1110,101 @@ inline int grid_for(long long total, int threads, int cap = 148 * 16) {
     return (int)g;
 }
 
+
+// Fast plans: N -> (N1, N2) with N1 % N2 == 0.
+#define BNF_FAST_PLANS(X) \
+    X(8, 4, 2) X(12, 6, 2) X(16, 4, 4) X(24, 12, 2) X(32, 8, 4) X(48, 12, 4) X(64, 8, 8) X(96, 24, 4) \
+    X(128, 16, 8) X(192, 24, 8) X(256, 16, 16)
+
+constexpr int zW(int N, int N2) { return N2 == 2 ? 16 : (N <= 128 ? 8 : 4); }
+constexpr int xR(int N2) { return N2 <= 8 ? 16 : 8; }
+constexpr int yW() { return 16; }
+
+bool has_fast(int N) {
+    switch (N) {
+#define BNF_CASE(NN, A, B) case NN: return true;
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return false;
+    }
+}
+
+template <class F, class... Args>
+cudaError_t launch_k(F f, dim3 g, int threads, size_t sm, cudaStream_t st, Args... args) {
+    if (sm > 32 * 1024) {   // leave room for the kernels' static shared memory
+        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    f<<<g, threads, sm, st>>>(args...);
+    return cudaGetLastError();
+}
+
+cudaError_t fast_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st,
+                      double2* Pcg = nullptr, const CGFuse* cg = nullptr) {
+    switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B)                                                                              \
+    case NN: {                                                                                          \
+        constexpr int W = zW(NN, B);                                                                       \
+        return cg ? launch_k(k_zfwd_fast<A, B, W, 1>, dim3((a.mp.n1 + W - 1) / W, a.mp.n2, nvec), 3 * W * B, \
+                             (size_t)3 * NN * W * sizeof(double2), st, Y, U, a, op, Pcg, *cg)             \
+                  : launch_k(k_zfwd_fast<A, B, W, 0>, dim3((a.mp.n1 + W - 1) / W, a.mp.n2, nvec), 3 * W * B, \
+                             (size_t)3 * NN * W * sizeof(double2), st, Y, U, a, op, Pcg, CGFuse{});       \
+    }
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+cudaError_t fast_zadj(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, cudaStream_t st,
+                      const CGFuse* cg = nullptr) {
+    switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B)                                                                              \
+    case NN: {                                                                                          \
+        constexpr int W = zW(NN, B);                                                                       \
+        return cg ? launch_k(k_zadj_fast<A, B, W, 1>, dim3((a.mp.n1 + W - 1) / W, a.mp.n2, nvec), 3 * W * B, \
+                             (size_t)3 * NN * W * sizeof(double2), st, U, OUT, a, op, *cg)                \
+                  : launch_k(k_zadj_fast<A, B, W, 0>, dim3((a.mp.n1 + W - 1) / W, a.mp.n2, nvec), 3 * W * B, \
+                             (size_t)3 * NN * W * sizeof(double2), st, U, OUT, a, op, CGFuse{});          \
+    }
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+cudaError_t fast_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaStream_t st) {
+    switch (a.mp.n2) {
+#define BNF_CASE(NN, A, B)                                                                                    \
+    case NN: {                                                                                                \
+        constexpr int W = yW();                                                                               \
+        dim3 g((a.mp.n1 + W - 1) / W, a.mp.n3, nvec > 0 ? 3 * nvec : 1);                                      \
+        const size_t sm = (size_t)fast::XchW<A, B, W>::size * sizeof(double2);                               \
+        return adjoint ? launch_k(k_ypass_fast<A, B, W, 1>, g, W * B, sm, st, U, a)                           \
+                       : launch_k(k_ypass_fast<A, B, W, 0>, g, W * B, sm, st, U, a);                          \
+    }
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+cudaError_t fast_xpass(const OpArgs& a, double2* U, int nvec, cudaStream_t st, const CGFuse* cg = nullptr) {
+    switch (a.mp.n1) {
+#define BNF_CASE(NN, A, B)                                                                                    \
+    case NN: {                                                                                                \
+        constexpr int R = xR(B);                                                                              \
+        const long long rows = (long long)a.mp.n2 * a.mp.n3;                                                  \
+        dim3 g((unsigned)((rows + R - 1) / R), nvec > 0 ? 3 * nvec : 1);                                      \
+        const size_t sm = (size_t)fast::XchT<A, B, R>::size * sizeof(double2);                               \
+        return cg ? launch_k(k_xpass_fast<A, B, R, 1>, g, R * B, sm, st, U, a, *cg)                           \
+                  : launch_k(k_xpass_fast<A, B, R, 0>, g, R * B, sm, st, U, a, CGFuse{});                     \
+    }
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -726,11 +1213,12 @@ static size_t smem_y(const OpArgs& a) { return (size_t)2 * a.mp.n2 * a.W_y * siz
 static size_t smem_x(const OpArgs& a) { return (size_t)2 * a.mp.n1 * (a.R_x + 1) * sizeof(double2); }
 
 static cudaError_t set_smem(const void* f, size_t bytes) {
-    if (bytes > 48 * 1024) return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (bytes > 32 * 1024) return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     return cudaSuccess;
 }
 
 cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st) {
+    if (a.fast && has_fast(a.mp.n3)) return fast_zfwd(a, Y, U, nvec, op, st);
     const size_t sm = smem_z(a);
     cudaError_t e = set_smem((const void*)k_zfwd, sm);
     if (e != cudaSuccess) return e;
@@ -740,6 +1228,7 @@ cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec,
 }
 
 cudaError_t launch_zadj(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, cudaStream_t st) {
+    if (a.fast && has_fast(a.mp.n3)) return fast_zadj(a, U, OUT, nvec, op, st);
     const size_t sm = smem_z(a);
     cudaError_t e = set_smem((const void*)k_zadj, sm);
     if (e != cudaSuccess) return e;
@@ -749,6 +1238,7 @@ cudaError_t launch_zadj(const OpArgs& a, const double2* U, double2* OUT, int nve
 }
 
 cudaError_t launch_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaStream_t st) {
+    if (a.fast && has_fast(a.mp.n2)) return fast_ypass(a, U, nvec, adjoint, st);
     const size_t sm = smem_y(a);
     dim3 g((a.mp.n1 + a.W_y - 1) / a.W_y, a.mp.n3, 3 * nvec);
     if (adjoint) {
@@ -764,6 +1254,7 @@ cudaError_t launch_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cud
 }
 
 cudaError_t launch_xpass(const OpArgs& a, double2* U, int nvec, cudaStream_t st) {
+    if (a.fast && has_fast(a.mp.n1)) return fast_xpass(a, U, nvec, st);
     const size_t sm = smem_x(a);
     cudaError_t e = set_smem((const void*)k_xpass, sm);
     if (e != cudaSuccess) return e;
@@ -873,6 +1364,35 @@ cudaError_t launch_cg_scalars(const CGState& s, const double2* rrnew_c, int nvec
 cudaError_t launch_cg_p(double2* P, const double2* R, const CGState& s, long long N, int nvec, cudaStream_t st) {
     k_cg_p<<<dim3(grid_for(N, 256, 148 * 4), nvec), 256, 0, st>>>(P, R, s, N);
     return cudaGetLastError();
+}
+
+
+bool fast_all(const OpArgs& a) { return a.fast && has_fast(a.mp.n1) && has_fast(a.mp.n2) && has_fast(a.mp.n3); }
+
+cudaError_t launch_zfwd_cg(const OpArgs& a, const double2* R, double2* P, double2* U, int nvec, const CGFuse& cg,
+                           cudaStream_t st) {
+    return fast_zfwd(a, R, U, nvec, 1, st, P, &cg);
+}
+cudaError_t launch_xpass_cg(const OpArgs& a, double2* U, int nvec, const CGFuse& cg, cudaStream_t st) {
+    return fast_xpass(a, U, nvec, st, &cg);
+}
+cudaError_t launch_zadj_cg(const OpArgs& a, const double2* U, double2* X, int nvec, const CGFuse& cg,
+                           cudaStream_t st) {
+    return fast_zadj(a, U, X, nvec, 1, st, &cg);
+}
+size_t cg_partials_per_vec(const OpArgs& a) {
+    const long long rows = (long long)a.mp.n2 * a.mp.n3;
+    const long long gx = (rows + 7) / 8;            // x pass: >= rows / R for every plan (R >= 8)
+    const long long gz = ((a.mp.n1 + 3) / 4) * (long long)a.mp.n2;   // z pass: W >= 4
+    return (size_t)std::max(3 * gx, gz);
+}
+
+
+cudaError_t launch_ypass_slab(const OpArgs& a, double2* U, int adjoint, cudaStream_t st) {
+    return fast_ypass(a, U, 0, adjoint, st);
+}
+cudaError_t launch_xpass_slab(const OpArgs& a, double2* U, const CGFuse* cg, cudaStream_t st) {
+    return fast_xpass(a, U, 0, st, cg);
 }
 
 }  // namespace bnf

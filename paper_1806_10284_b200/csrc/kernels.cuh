@@ -45,21 +45,54 @@ struct OpArgs {
     TwP tw;
     AxisPlan px, py, pz;
     const double* eps_inv;   // [3][n]  1/eps at the Yee points
+    const unsigned char* eps_idx;  // [3][n] index into eps_lut (compressed B^{-1}), or null
+    const double* eps_lut;   // <= 256 distinct values of 1/eps
     double inv_n;
-    int W_z, W_y, R_x;       // tile widths
+    int W_z, W_y, R_x;       // tile widths (generic Stockham path)
+    int fast;                // 1: register-FFT fast path where the axis length has a plan
+    int comp0;               // first component slab (vector*3 + l) of a split y/x launch
+    int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
 };
 
 struct Profiler;  // host-side, see solver.cu
 
+// Fused-CG state (device pointers): the operator passes of one CG
+// iteration also do p = r + beta p (zfwd), (p, M p) and alpha (x pass) and
+// x += alpha p, r -= alpha M p, (r, r), beta (zadj).
+struct CGFuse {
+    double2* P;
+    double2* R;
+    double* part_x;           // [nvec][partials]
+    double* part_z;
+    unsigned int* counter;    // [2], zero between launches
+    double* rr;
+    double* pmp;
+    double* alpha;
+    double* beta;
+    double* thr;
+    int* active;
+};
+
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
 cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st);
 cudaError_t launch_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaStream_t st);
+// one component slab (vector*3 + l = a.comp0) of the y / x passes
+cudaError_t launch_ypass_slab(const OpArgs& a, double2* U, int adjoint, cudaStream_t st);
+cudaError_t launch_xpass_slab(const OpArgs& a, double2* U, const CGFuse* cg, cudaStream_t st);
 cudaError_t launch_xpass(const OpArgs& a, double2* U, int nvec, cudaStream_t st);
 cudaError_t launch_zadj(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, cudaStream_t st);
 cudaError_t launch_xfwd_recover(const OpArgs& a, double2* U, int nvec, const double* eps_inv, double scale0,
                                 const double* scales, cudaStream_t st);
 cudaError_t launch_bloch_phase(const OpArgs& a, double2* U, int nvec, double kap1, double kh2, double kh3,
                                cudaStream_t st);
+
+bool fast_all(const OpArgs& a);
+cudaError_t launch_zfwd_cg(const OpArgs& a, const double2* R, double2* P, double2* U, int nvec, const CGFuse& cg,
+                           cudaStream_t st);
+cudaError_t launch_xpass_cg(const OpArgs& a, double2* U, int nvec, const CGFuse& cg, cudaStream_t st);
+cudaError_t launch_zadj_cg(const OpArgs& a, const double2* U, double2* X, int nvec, const CGFuse& cg,
+                           cudaStream_t st);
+size_t cg_partials_per_vec(const OpArgs& a);
 
 cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st);
 

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -169,7 +170,7 @@ struct bnf_solver {
     long long n = 0;
     OpArgs args{};
     DevBuf root[3], twlo, twhi;
-    DevBuf eps_inv;
+    DevBuf eps_inv, eps_idx, eps_lut;
     bool eps_set = false;
     DevBuf sigma;
     bool kappa_set = false;
@@ -181,6 +182,10 @@ struct bnf_solver {
     DevBuf small;    // small device scalars/matrices
     DevBuf cgstate;
     CGState cgs{};
+    DevBuf cgfuse_buf;
+    CGFuse cgf{};
+    bool fused_ok = false;
+    bool l2_slabs = false;
     DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
     int nev_last = 0;
@@ -323,13 +328,71 @@ int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_o
     return BNF_OK;
 }
 
+// Same CG with the vector updates and reductions fused into the operator
+// passes (kernels.cu: zfwd p-update, x-pass (p,Mp)/alpha, zadj x/r update,
+// (r,r)/beta).  Used when every axis has a register-FFT plan.
+int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
+    const long long N = 2 * s->n;
+    const size_t vb = (size_t)N * nvec * sizeof(double2);
+    CK(s->cgr.ensure(vb));
+    CK(s->cgp.ensure(vb));
+    TRY(ensure_work(s, nvec));
+    double2* R = s->cgr.as<double2>();
+    double2* P = s->cgp.as<double2>();
+    double2* U = s->U.as<double2>();
+    double2* dd = s->small.as<double2>();
+    CK(cudaMemsetAsync(X, 0, vb, s->st));
+    CK(cudaMemsetAsync(P, 0, vb, s->st));
+    RUN("copy", launch_copy(R, C, N * nvec, s->st));
+    TRY(dots(s, R, R, N, nvec, dd));
+    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->o.tol_inner, s->st));
+    CK(cudaMemsetAsync(s->cgs.beta, 0, nvec * sizeof(double), s->st));
+    CGFuse cg = s->cgf;
+    cg.P = P;
+    cg.R = R;
+    int it = 0;
+    for (; it < s->o.max_inner; ++it) {
+        RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
+        if (s->l2_slabs) {
+            // y -> x -> y per component slab: the slab stays resident in L2 between the passes
+            OpArgs sa = s->args;
+            sa.nvec_all = nvec;
+            for (int vl = 0; vl < 3 * nvec; ++vl) {
+                sa.comp0 = vl;
+                RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
+                RUN("xpass_cg", launch_xpass_slab(sa, U, &cg, s->st));
+                RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
+            }
+        } else {
+            RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
+            RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
+            RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
+        }
+        RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
+        s->matvecs += nvec;
+        CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        if (s->prof.on) s->prof.flush();
+        int act = 0;
+        for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
+        if (act == 0) {
+            ++it;
+            break;
+        }
+    }
+    s->inner_iters += (long long)it * nvec;
+    if (iters_out) *iters_out = it;
+    return BNF_OK;
+}
+
 // Y = Sigma^{-1} CG(M, Sigma^{-1} X)  =  A_r^{-1} X
 int apply_Ar_inv(bnf_solver* s, const double2* X, double2* Y, int nvec) {
     const long long N = 2 * s->n;
     CK(s->cgc.ensure((size_t)N * nvec * sizeof(double2)));
     double2* C = s->cgc.as<double2>();
     RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->n, nvec, 1, s->st));
-    TRY(cg_solve(s, C, Y, nvec, nullptr));
+    if (s->fused_ok) TRY(cg_solve_fused(s, C, Y, nvec, nullptr));
+    else TRY(cg_solve(s, C, Y, nvec, nullptr));
     RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->n, nvec, 1, s->st));
     return BNF_OK;
 }
@@ -626,6 +689,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     p.gamma = -1;
     p.taup = 1e-6;
     s->args.inv_n = 1.0 / (double)n;
+    s->args.fast = (std::getenv("BNF_NO_FAST") == nullptr) ? 1 : 0;
     // tile widths: keep each kernel's shared memory <= ~100 KB
     const int budget = 100 * 1024;
     s->args.W_z = std::max(1, std::min(16, pow2_floor(budget / (4 * 16 * n3))));
@@ -651,6 +715,25 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         s->cgs.pMp = (double2*)(b + 384 * 8);
     }
     CK(cudaMallocHost((void**)&s->h_flags, 64 * sizeof(int)));
+    s->fused_ok = fast_all(s->args) && std::getenv("BNF_NO_FUSED_CG") == nullptr;
+    s->l2_slabs = s->fused_ok && std::getenv("BNF_L2_SLABS") != nullptr;
+    if (s->fused_ok) {
+        const size_t per = cg_partials_per_vec(s->args);
+        const size_t bytes = 2 * 8 * per * sizeof(double) + 4 * 64 * sizeof(double) + 64;
+        CK(s->cgfuse_buf.ensure(bytes));
+        CK(cudaMemset(s->cgfuse_buf.p, 0, bytes));
+        char* b = s->cgfuse_buf.as<char>();
+        s->cgf.part_x = (double*)b;
+        s->cgf.part_z = (double*)(b + 8 * per * sizeof(double));
+        char* c = b + 2 * 8 * per * sizeof(double);
+        s->cgf.pmp = (double*)c;
+        s->cgf.alpha = (double*)(c + 64 * sizeof(double));
+        s->cgf.counter = (unsigned int*)(c + 4 * 64 * sizeof(double));
+        s->cgf.rr = s->cgs.rr;
+        s->cgf.beta = s->cgs.beta;
+        s->cgf.thr = s->cgs.thr;
+        s->cgf.active = s->cgs.active;
+    }
     *out = s.release();
     return BNF_OK;
 }
@@ -685,6 +768,33 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
         h[t] = 1.0 / h[t];
     }
     CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), n3 * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    // Compressed copy for the hot x pass: uint8 index + LUT when <= 256 distinct values
+    // (exact: the LUT holds the same doubles).
+    std::map<double, int> lut;
+    bool small = true;
+    for (long long t = 0; t < n3 && small; ++t) {
+        if (lut.find(h[t]) == lut.end()) {
+            if (lut.size() >= 256) small = false;
+            else lut.emplace(h[t], 0);
+        }
+    }
+    s->args.eps_idx = nullptr;
+    s->args.eps_lut = nullptr;
+    if (small && std::getenv("BNF_NO_EPS_LUT") == nullptr) {
+        std::vector<double> vals;
+        for (auto& kv : lut) {
+            kv.second = (int)vals.size();
+            vals.push_back(kv.first);
+        }
+        std::vector<unsigned char> idx(n3);
+        for (long long t = 0; t < n3; ++t) idx[t] = (unsigned char)lut[h[t]];
+        CK(s->eps_idx.ensure(n3));
+        CK(s->eps_lut.ensure(256 * sizeof(double)));
+        CK(cudaMemcpyAsync(s->eps_idx.p, idx.data(), n3, cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemcpyAsync(s->eps_lut.p, vals.data(), vals.size() * sizeof(double), cudaMemcpyHostToDevice, s->st));
+        s->args.eps_idx = s->eps_idx.as<unsigned char>();
+        s->args.eps_lut = s->eps_lut.as<double>();
+    }
     CK(cudaStreamSynchronize(s->st));
     s->eps_set = true;
     return BNF_OK;

@@ -241,3 +241,23 @@ def test_full_size_eigenpairs_residual(bnf, idx, kidx):
         assert r <= 1e-8, (i, r)
         rq = np.vdot(Y[i], Ay).real / nrm ** 2
         assert abs(rq - lam[i]) <= 1e-10 * lam[i]
+
+
+def _full_goldens():
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(f for f in os.listdir(gdir) if f.startswith("full_c") and f.endswith("_oracle.json"))
+
+
+@pytest.mark.parametrize("fname", _full_goldens())
+def test_full_size_eigenvalues_vs_oracle(bnf, golden_dir, fname):
+    """BASELINE configs at their FULL grids (k-subsets incl. Gamma): the nev
+    smallest eigenvalues equal the oracle's (scripts/make_golden_full.py:
+    oracle inverse Lanczos + CG on the numpy Algorithms-1/2 operator) to
+    1e-10 relative -- the north-star eigenvalue bar."""
+    g = _golden(golden_dir, fname)
+    cfg = configs.config(g["config"])
+    L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape)
+    h = __import__("hashlib").sha256(np.concatenate([np.ravel(e) for e in eps]).tobytes()).hexdigest()[:16]
+    assert h == g["eps_sha256_16"]
+    lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
