@@ -3,7 +3,7 @@ only: every step of the hot path runs in libbnf.so's CUDA kernels).
 
 The package deliberately has NO fallback: if libbnf.so is missing or fails
 to load, importing this module raises.  Build it with
-``python -m paper_1806_10284_b200.build`` (or ``__graft_entry__.build()``).
+``python paper_1806_10284_b200/build.py`` (or ``__graft_entry__.build()``).
 """
 from __future__ import annotations
 
@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbnf.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError("libbnf.so not built (%s); run python -m paper_1806_10284_b200.build" % LIB_PATH)
+    raise ImportError("libbnf.so not built (%s); run python paper_1806_10284_b200/build.py" % LIB_PATH)
 _lib = C.CDLL(LIB_PATH)
 
 OK, EINVAL, EGEOM, ENOMEM, ECUDA, ENCCL, ENOCONV, ESTATE = range(8)

@@ -1,7 +1,9 @@
 """In-tree build of libbnf.so (sm_100a) with nvcc.
 
-    python -m paper_1806_10284_b200.build        # incremental
-    python -m paper_1806_10284_b200.build --force
+    python paper_1806_10284_b200/build.py        # incremental
+    python paper_1806_10284_b200/build.py --force
+
+(run by path: importing the package requires the library it builds)
 """
 from __future__ import annotations
 

@@ -1,0 +1,7 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python paper_1806_10284_b200/build.py > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench rc=$?
+timeout 600 python scripts/bench_apply.py > gpurun_out/bench_apply.log 2>&1; echo apply rc=$?
