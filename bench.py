@@ -47,6 +47,14 @@ PASS_BYTES = {
     "zfwd_cg": lambda n: 4 * 16 * n + 2 * 16 * n + 3 * 16 * n,   # read r,p; write p; write 3 components
     "xpass_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     "zadj_cg": lambda n: 3 * 16 * n + 2 * 16 * n + 8 * 16 * n,   # read U, p; read+write x, r
+    # fused y/x/y plane pass (plane.cu): one read + write of U, eps as uint8
+    "plane": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    "plane_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    # persistent pipelined z passes (zpass.cu); CG x update deferred into zfwd2_cg
+    "zfwd2": lambda n: 2 * 16 * n + 3 * 16 * n,
+    "zadj2": lambda n: 3 * 16 * n + 2 * 16 * n,
+    "zfwd2_cg": lambda n: 6 * 16 * n + 4 * 16 * n + 3 * 16 * n,   # read r,p,x; write p,x; write U
+    "zadj2_cg": lambda n: 3 * 16 * n + 4 * 16 * n,                 # read U, r; write r
 }
 
 
@@ -281,19 +289,22 @@ def main():
     n = lat.nn
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else None
     # vectors served by the CG-fused passes vs the plain ones (plain y/x passes serve both)
-    mv_cg = mv
-    if "zfwd_cg" in ktimes and "zfwd" in ktimes and ktimes["zfwd"][1] + ktimes["zfwd_cg"][1] > 0:
-        mv_cg = mv * ktimes["zfwd_cg"][1] / (ktimes["zfwd"][1] + ktimes["zfwd_cg"][1])
-    elif "zfwd_cg" not in ktimes:
-        mv_cg = 0
+    zc = sum(v[1] for k, v in ktimes.items() if k.startswith("zfwd") and k.endswith("_cg"))
+    zp = sum(v[1] for k, v in ktimes.items() if k.startswith("zfwd") and not k.endswith("_cg"))
+    mv_cg = mv * zc / (zc + zp) if zc + zp > 0 else 0
+    def vecs(k):   # vectors served by pass k ("_cg" variants serve CG iterations only)
+        if k.endswith("_cg"):
+            return mv_cg
+        if k + "_cg" in PASS_BYTES:
+            return mv - mv_cg
+        return mv
     roof = None
     if dom and dom[0] in PASS_BYTES:
         name, (kms, kcnt) = dom
         per_vec = PASS_BYTES[name](n)
         # every apply launches each pass once per batch: the pass's vector count is
         # the matvecs it served (fused-CG and plain variants are timed separately)
-        mv_kernel = mv if not name.endswith("_cg") else mv_cg
-        total_bytes = per_vec * mv_kernel
+        total_bytes = per_vec * vecs(name)
         achieved = total_bytes / (kms / 1000.0) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -305,8 +316,7 @@ def main():
                 "avg_launch_us": 1000.0 * kms / kcnt, "peak_source": peak_src,
                 "share_of_step": kms / ms}
     matvec_ms = sum(v[0] for k, v in ktimes.items() if k in PASS_BYTES)
-    matvec_bytes = sum(PASS_BYTES[k](n) * (mv_cg if k.endswith("_cg") else (mv - mv_cg if k.startswith("z") else mv))
-                       for k in ktimes if k in PASS_BYTES)
+    matvec_bytes = sum(PASS_BYTES[k](n) * vecs(k) for k in ktimes if k in PASS_BYTES)
     cpu = None
     if not args.no_cpu and world >= 1:
         r, c, dt = oracle_rate(cfg)

@@ -1,0 +1,90 @@
+// Block reductions and the fused-CG scalar updates shared by the operator
+// passes (kernels.cu, plane.cu).  Internal.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace bnf {
+namespace {
+
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    return v;
+}
+
+// block-wide sum of one complex value (blockDim.x multiple of 32, <= 1024)
+__device__ double2 block_sum(double2 v, double2* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    __syncthreads();
+    if (ln == 0) red[w] = v;
+    __syncthreads();
+    double2 r = make_double2(0, 0);
+    if (w == 0) {
+        r = (ln < (int)(blockDim.x >> 5)) ? red[ln] : make_double2(0, 0);
+        r = warp_sum(r);
+    }
+    return r;  // valid in thread 0
+}
+
+// ---------------------------------------------- fused-CG reductions
+// Block partial of one double (written by thread 0), then a "last block
+// done" election; the last block reduces all partials in a fixed order
+// (deterministic) and updates the CG scalars.
+__device__ void cg_block_partial(double v, double* slot, double2* scratch) {
+    __syncthreads();   // scratch (shared memory) may still be in use
+    const double2 s = block_sum(make_double2(v, 0.0), scratch);
+    if (threadIdx.x == 0) *slot = s.x;
+}
+__device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2* scratch) {
+    __shared__ int is_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter, 1u);
+        is_last = (prev == total - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last != 0;
+}
+__device__ double block_sum_fixed(const double* part, int nb, double2* scratch) {
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) acc += ((volatile const double*)part)[t];
+    __syncthreads();
+    const double2 s = block_sum(make_double2(acc, 0.0), scratch);
+    __shared__ double res;
+    if (threadIdx.x == 0) res = s.x;
+    __syncthreads();
+    return res;
+}
+__device__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+    for (int v = 0; v < nvec; ++v) {
+        const double pmp = block_sum_fixed(cg.part_x + (size_t)v * nb, nb, scratch);
+        if (threadIdx.x == 0) {
+            cg.pmp[v] = pmp;
+            cg.alpha[v] = (cg.active[v] && pmp > 0.0) ? cg.rr[v] / pmp : 0.0;
+        }
+    }
+    if (threadIdx.x == 0) cg.counter[0] = 0u;
+}
+__device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+    for (int v = 0; v < nvec; ++v) {
+        const double rn = block_sum_fixed(cg.part_z + (size_t)v * nb, nb, scratch);
+        if (threadIdx.x == 0) {
+            const int act = cg.active[v];
+            cg.beta[v] = (act && cg.rr[v] > 0.0) ? rn / cg.rr[v] : 0.0;
+            if (act) cg.rr[v] = rn;
+            cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;
+        }
+    }
+    if (threadIdx.x == 0) cg.counter[1] = 0u;
+}
+
+}  // namespace
+}  // namespace bnf

@@ -52,6 +52,7 @@ struct OpArgs {
     int fast;                // 1: register-FFT fast path where the axis length has a plan
     int comp0;               // first component slab (vector*3 + l) of a split y/x launch
     int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
+    const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -93,6 +94,23 @@ cudaError_t launch_xpass_cg(const OpArgs& a, double2* U, int nvec, const CGFuse&
 cudaError_t launch_zadj_cg(const OpArgs& a, const double2* U, double2* X, int nvec, const CGFuse& cg,
                            cudaStream_t st);
 size_t cg_partials_per_vec(const OpArgs& a);
+
+// Fused real-space plane pass (plane.cu): y-DFT, twiddle, x-DFT, B^{-1},
+// x-DFT*, twiddle*, y-DFT* on every (component, z-plane) of nslab = 3*nvec
+// component slabs, one HBM read + write.  Square xy planes with a fast plan.
+bool plane_supported(const OpArgs& a);
+
+// Persistent, cp.async-pipelined z passes (zpass.cu).  cg == nullptr: plain
+// op (0 = A_r, 1 = M); otherwise the CG-fused variants (x update deferred:
+// zfwd2 does x += alpha_prev p, p <- r + beta p; zadj2 does r -= alpha M p and
+// the (r,r)/beta reduction; finish with launch_cg_xfinal).
+bool zpass2_supported(const OpArgs& a);
+cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, double2* P, double2* X,
+                         const CGFuse* cg, cudaStream_t st);
+cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,
+                         cudaStream_t st);
+cudaError_t launch_cg_xfinal(double2* X, const double2* P, const double* alpha, long long N, int nvec, cudaStream_t st);
+cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st);
 
 cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st);
 

@@ -1,0 +1,240 @@
+// Fused real-space plane pass of the null-space-free matvec (SURVEY.md §8(a)
+// a2-a4, Algorithms 1-2 of PAPER.md §5.3):
+//
+//   for every component l and z-plane c of U (x-fastest, rows of n1):
+//     y-DFT over j (+)         (Alg. 2 step 2)
+//     twiddle e^{-2 pi i b m1 i / (n1 n2)}
+//     x-DFT over i (+)         (Alg. 2 step 3)
+//     * 1/(n eps_l(a,b,c))     (B^{-1}; T^* B^{-1} T with un-normalised DFTs, DESIGN R7b)
+//     x-DFT over a (-)         (Alg. 1 step 1)
+//     twiddle e^{+2 pi i b m1 i / (n1 n2)}
+//     y-DFT over b (-)         (Alg. 1 step 2)
+//
+// in ONE read and ONE write of the plane (96n B + 3n B of eps per vector
+// instead of 3 x 96n for separate y / x / y passes).  A plane of N x N
+// complex128 is split over a thread-block cluster of P = N/32 CTAs (P = 1
+// for N <= 48): CTA r owns columns [32r, 32r+32) for the y phases and rows
+// [32r, 32r+32) for the x phase; the two layouts are exchanged through
+// distributed shared memory (st.shared::cluster), so the transpose never
+// touches HBM.  Each FFT is the register-resident two-stage N1 x N2 plan of
+// fastfft.cuh (shared-memory transpose inside the CTA).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "cgfuse.cuh"
+#include "fastfft.cuh"
+#include "kernels.cuh"
+
+namespace cgx = cooperative_groups;
+
+namespace bnf {
+namespace {
+
+using fast::cmul;
+using fast::cscale;
+
+__device__ __forceinline__ double2 tw_at(const TwP& t, unsigned long long P) {  // e^{2 pi i P / n}
+    return cmul(__ldg(t.hi + (P >> t.shift)), __ldg(t.lo + (P & t.mask)));
+}
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+
+template <int P>
+struct Cluster {
+    __device__ static unsigned rank() { return P == 1 ? 0u : cgx::this_cluster().block_rank(); }
+    __device__ static void sync() {
+        if (P == 1) __syncthreads();
+        else cgx::this_cluster().sync();
+    }
+    __device__ static double2* map(double2* p, unsigned r) {
+        return P == 1 ? p : cgx::this_cluster().map_shared_rank(p, r);
+    }
+};
+
+// smem (complex elements): max(N * CW data, XchT exchange) = CW * N1 * (N2 + 1)
+template <int N1, int N2, int P>
+struct PlaneCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int CW = N / P;     // columns (y phases) = rows (x phase) per CTA
+    static constexpr int NT = CW * N2;   // threads
+    static constexpr int SMEM = CW * N1 * (N2 + 1);
+};
+
+template <int N1, int N2, int P, int CG>
+__global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
+    using C = PlaneCfg<N1, N2, P>;
+    constexpr int N = C::N, CW = C::CW;
+    extern __shared__ double2 D[];
+    __shared__ double2 red[32];
+    const ModeP& p = a.mp;
+    const unsigned r = Cluster<P>::rank();
+    const int c = blockIdx.x / P;
+    const int vl = blockIdx.y + a.comp0;
+    const int l = vl % 3;
+    const int tid = threadIdx.x;
+    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    double2 v[N1];
+
+    // ---------------- phase Y: columns i = r*CW + w, FFT over j ----------------
+    const int w = tid % CW, t = tid / CW;
+    const int i = (int)r * CW + w;
+    // integer phase numerators mod n12 (n1 n2 <= 2^20: 32-bit arithmetic is exact)
+    const unsigned n12 = (unsigned)p.n12;
+    const unsigned long long s3 = (unsigned long long)p.n3;
+    const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;   // m1 i mod n12
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+    fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+    {
+        // e^{-2 pi i b M / n12} for b = t + N2 u + N1 k2: w^t (w^N2)^u (w^N1)^k2
+        const unsigned Pt = ((unsigned)t * M) % n12;
+        const unsigned Pu = ((unsigned)N2 * M) % n12;
+        const unsigned Pk = ((unsigned)N1 * M) % n12;
+        const double2 wt = conj2(tw_at(a.tw, Pt * s3));
+        const double2 wu = conj2(tw_at(a.tw, Pu * s3));
+        const double2 wk = conj2(tw_at(a.tw, Pk * s3));
+        double2 au = wt;
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u) {
+            double2 f = au;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                v[u * N2 + k2] = cmul(v[u * N2 + k2], f);
+                f = cmul(f, wk);
+            }
+            au = cmul(au, wu);
+        }
+    }
+    // exchange Y -> X: element (b, i) goes to CTA b / CW, row b % CW, column i
+    Cluster<P>::sync();   // every CTA is done with its own D
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            const int b = t + N2 * u + N1 * k2;
+            double2* dst = Cluster<P>::map(D, (unsigned)(b / CW));
+            dst[(b % CW) * N + i] = v[u * N2 + k2];
+        }
+    Cluster<P>::sync();
+
+    // ---------------- phase X: rows b = r*CW + rw, FFT over i ----------------
+    const int tx = tid % N2, rw = tid / N2;
+    const int b = (int)r * CW + rw;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v[m] = D[rw * N + N2 * m + tx];
+    __syncthreads();   // D becomes the transpose buffer
+    fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    double pmp = 0.0;
+    {
+        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int aa = tx + N2 * u + N1 * k2;
+                const double e_ = a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
+                                            : __ldg(a.eps_inv + rowofs + aa);
+                const double s_ = a.inv_n * e_;
+                const double2 x = v[u * N2 + k2];
+                if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
+                v[u * N2 + k2] = cscale(x, s_);
+            }
+    }
+    if (CG) {
+        // per-vector partial of (p, M p); the last CTA of the launch forms alpha
+        const int vec = vl / 3;
+        const int nb = gridDim.x * 3;
+        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
+        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, red);
+        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, red)) cg_finish_alpha(cgf, nb, nvec_all, red);
+    }
+    fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    // exchange X -> Y: element (b, a) goes to CTA a / CW, row b, column a % CW (ld CW)
+    Cluster<P>::sync();
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+        const int aa = N2 * m + tx;
+        double2* dst = Cluster<P>::map(D, (unsigned)(aa / CW));
+        dst[b * CW + (aa % CW)] = v[m];
+    }
+    Cluster<P>::sync();
+
+    // ---------------- phase Y*: conj twiddle, FFT (-) over b ----------------
+    {
+        // e^{+2 pi i b M / n12} for b = N2 m + t: w^t (w^N2)^m
+        const unsigned Pt = ((unsigned)t * M) % n12;
+        const unsigned Pu = ((unsigned)N2 * M) % n12;
+        double2 f = tw_at(a.tw, Pt * s3);
+        const double2 wu = tw_at(a.tw, Pu * s3);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+            v[m] = cmul(D[(N2 * m + t) * CW + w], f);
+            f = cmul(f, wu);
+        }
+    }
+    __syncthreads();
+    fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            const int j = t + N2 * u + N1 * k2;
+            plane[(size_t)j * N + i] = v[u * N2 + k2];
+        }
+}
+
+template <int N1, int N2, int P>
+cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    using C = PlaneCfg<N1, N2, P>;
+    const size_t smem = (size_t)C::SMEM * sizeof(double2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P * a.mp.n3), (unsigned)nslab, 1);
+    cfg.blockDim = dim3(C::NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = P > 1 ? 1 : 0;
+    auto run = [&](auto kern, auto cgarg) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (P > 8) {
+            e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg);
+    };
+    if (cg) return run(k_plane<N1, N2, P, 1>, *cg);
+    return run(k_plane<N1, N2, P, 0>, CGFuse{});
+}
+
+}  // namespace
+
+// Plans: N -> (N1, N2, P).  P = N/32 (32 columns per CTA) from N = 64 up.
+#define BNF_PLANE_PLANS(X) \
+    X(8, 4, 2, 1) X(12, 6, 2, 1) X(16, 4, 4, 1) X(24, 12, 2, 1) X(32, 8, 4, 1) X(48, 12, 4, 1) \
+    X(64, 8, 8, 2) X(96, 24, 4, 3) X(128, 16, 8, 4) X(192, 24, 8, 6) X(256, 16, 16, 8)
+
+bool plane_supported(const OpArgs& a) {
+    if (!a.fast || a.mp.n1 != a.mp.n2) return false;
+    switch (a.mp.n1) {
+#define BNF_CASE(NN, A, B, PP) case NN: return true;
+        BNF_PLANE_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return false;
+    }
+}
+
+cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    switch (a.mp.n1) {
+#define BNF_CASE(NN, A, B, PP) case NN: return launch_plane_t<A, B, PP>(a, U, nslab, cg, st);
+        BNF_PLANE_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace bnf

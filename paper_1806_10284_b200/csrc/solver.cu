@@ -186,6 +186,9 @@ struct bnf_solver {
     CGFuse cgf{};
     bool fused_ok = false;
     bool l2_slabs = false;
+    bool use_plane = false;   // fused y/x/y plane pass (plane.cu)
+    bool use_z2 = false;      // persistent pipelined z passes (zpass.cu)
+    DevBuf hroot;             // e^{i pi k / n3}
     DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
     int nev_last = 0;
@@ -259,11 +262,17 @@ int ensure_work(bnf_solver* s, int nvec) {
 int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     TRY(ensure_work(s, nvec));
     double2* U = s->U.as<double2>();
-    RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
-    RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
-    RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
-    RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
-    RUN("zadj", launch_zadj(s->args, U, out, nvec, op, s->st));
+    if (s->use_z2) RUN("zfwd2", launch_zfwd2(s->args, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
+    else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
+    if (s->use_plane) {
+        RUN("plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+    } else {
+        RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
+        RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
+        RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
+    }
+    if (s->use_z2) RUN("zadj2", launch_zadj2(s->args, U, out, nvec, op, nullptr, s->st));
+    else RUN("zadj", launch_zadj(s->args, U, out, nvec, op, s->st));
     s->matvecs += nvec;
     return BNF_OK;
 }
@@ -347,13 +356,17 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     TRY(dots(s, R, R, N, nvec, dd));
     RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->o.tol_inner, s->st));
     CK(cudaMemsetAsync(s->cgs.beta, 0, nvec * sizeof(double), s->st));
+    CK(cudaMemsetAsync(s->cgf.alpha, 0, nvec * sizeof(double), s->st));
     CGFuse cg = s->cgf;
     cg.P = P;
     cg.R = R;
     int it = 0;
     for (; it < s->o.max_inner; ++it) {
-        RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
-        if (s->l2_slabs) {
+        if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
+        else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
+        if (s->use_plane) {
+            RUN("plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+        } else if (s->l2_slabs) {
             // y -> x -> y per component slab: the slab stays resident in L2 between the passes
             OpArgs sa = s->args;
             sa.nvec_all = nvec;
@@ -368,7 +381,8 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
             RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
         }
-        RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
+        if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
+        else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
         s->matvecs += nvec;
         CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));
@@ -380,6 +394,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             break;
         }
     }
+    if (s->use_z2) RUN("cg_xfinal", launch_cg_xfinal(X, P, s->cgf.alpha, N, nvec, s->st));
     s->inner_iters += (long long)it * nvec;
     if (iters_out) *iters_out = it;
     return BNF_OK;
@@ -717,6 +732,15 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     CK(cudaMallocHost((void**)&s->h_flags, 64 * sizeof(int)));
     s->fused_ok = fast_all(s->args) && std::getenv("BNF_NO_FUSED_CG") == nullptr;
     s->l2_slabs = s->fused_ok && std::getenv("BNF_L2_SLABS") != nullptr;
+    s->use_plane = plane_supported(s->args) && std::getenv("BNF_NO_PLANE") == nullptr;
+    {
+        std::vector<double2> h(n3);
+        for (int k = 0; k < n3; ++k) h[k] = unit_root(k, 2LL * n3);
+        CK(s->hroot.ensure(n3 * sizeof(double2)));
+        CK(cudaMemcpy(s->hroot.p, h.data(), n3 * sizeof(double2), cudaMemcpyHostToDevice));
+        s->args.hroot_z = s->hroot.as<double2>();
+    }
+    s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     if (s->fused_ok) {
         const size_t per = cg_partials_per_vec(s->args);
         const size_t bytes = 2 * 8 * per * sizeof(double) + 4 * 64 * sizeof(double) + 64;

@@ -1,0 +1,481 @@
+// Fourier-side z passes of the null-space-free matvec, persistent and
+// software-pipelined (§5.3):
+//
+//   zfwd : Sigma_r, Pi combine (2 -> 3 components), z-DFT k -> c (+),
+//          twiddle e^{+2 pi i c N3(i,j)/n}                       (Alg. 2 step 1)
+//   zadj : conj twiddle, z-DFT c -> k (-), Pi^* combine (3 -> 2), Sigma_r
+//                                                                (Alg. 1 step 3)
+//
+// One CTA per SM loops over column tiles (W consecutive i, one j, all k).
+// The next tile's inputs stream into a second shared-memory stage with
+// cp.async while the current tile is computed, so HBM stays busy through
+// the FP64 mode algebra and the register FFTs.  Inter-axis twiddles are
+// products of three exact table entries (no per-element table gathers);
+// lambda3 along k comes from the column's half angle and an exact
+// e^{i pi k/n3} table (modes.cuh).
+//
+// CG-fused variants (cg_solve_fused, solver.cu), per iteration:
+//   zfwd_cg : x += alpha_prev p;  p <- r + beta p;  U = Q_r-side of p
+//   zadj_cg : r -= alpha M p;  partial (r, r);  the last CTA forms beta
+// (the x update is deferred by one iteration so that zadj touches only U
+// and r; the final update is k_cg_xfinal).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "cgfuse.cuh"
+#include "fastfft.cuh"
+#include "kernels.cuh"
+#include "modes.cuh"
+
+namespace bnf {
+namespace {
+
+using fast::cmul;
+using fast::cscale;
+using modes::Coef;
+using modes::Col;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+__device__ __forceinline__ double2 tw_at(const TwP& t, unsigned long long P) {  // e^{2 pi i P / n}
+    return cmul(__ldg(t.hi + (P >> t.shift)), __ldg(t.lo + (P & t.mask)));
+}
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cjm(double2 a, double2 b) {   // conj(a) b
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd3(double2 a, double2 b, double2 c) {
+    return make_double2(a.x + b.x + c.x, a.y + b.y + c.y);
+}
+
+template <int N1, int N2, int W>
+struct ZCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int NT = 3 * W * N2;
+    static constexpr int TE = N * W;                 // elements per array tile
+    static constexpr int S = (TE + NT - 1) / NT;      // elements per thread in the mode loops
+};
+
+struct ColS {   // per-column constants shared through smem
+    Col cm;
+    unsigned long long base3;   // N3(i, j) mod n
+};
+
+struct TileIdx {
+    int i0, j, vec;
+};
+__device__ __forceinline__ TileIdx tile_of(int tile, int nit, int n2) {
+    TileIdx t;
+    t.i0 = (tile % nit);
+    const int r = tile / nit;
+    t.j = r % n2;
+    t.vec = r / n2;
+    return t;
+}
+
+template <int W>
+__device__ __forceinline__ void col_setup(const ModeP& p, const TileIdx& ti, ColS* cs) {
+    if (threadIdx.x < W) {
+        const int i = ti.i0 * W + threadIdx.x;
+        cs[threadIdx.x].cm = modes::col(p, i, ti.j);
+        cs[threadIdx.x].base3 =
+            (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)ti.j) % p.n);
+    }
+}
+
+// ------------------------------------------------------------------ zfwd
+// MODE 0: U = Q_r Sigma_op Y (op = a runtime 0 A_r / 1 M).  MODE 1: CG (op M).
+template <int N1, int N2, int W, int MODE>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 1)
+    k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, int nvec, double2* __restrict__ Pcg,
+            double2* __restrict__ Xcg, CGFuse cg) {
+    using C = ZCfg<N1, N2, W>;
+    constexpr int N = C::N, NT = C::NT, TE = C::TE, S = C::S;
+    constexpr int NA = MODE ? 4 : 2;   // staged arrays: y1 y2 | r1 r2 p1 p2
+    extern __shared__ double2 sm[];
+    double2* stage = sm;                       // [2][NA][TE]
+    double2* Ct = sm + 2 * NA * TE;            // [3][TE] component tiles
+    double2* hroot = Ct + 3 * TE;              // [N]
+    __shared__ ColS cs[W];
+    const ModeP& p = a.mp;
+    const long long n = p.n;
+    const int n1 = p.n1, n2 = p.n2;
+    const int nit = n1 / W;
+    const int ntiles = nit * n2 * nvec;
+    const size_t kstride = (size_t)n1 * n2;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < N; k += NT) hroot[k] = __ldg(a.hroot_z + k);
+
+    auto issue = [&](int tile, int st) {
+        const TileIdx ti = tile_of(tile, nit, n2);
+        const size_t col0 = (size_t)ti.i0 * W + (size_t)n1 * ti.j;
+        double2* dst = stage + (size_t)st * NA * TE;
+#pragma unroll 1
+        for (int q = tid; q < TE; q += NT) {
+            const int k = q / W, w = q - k * W;
+            const size_t g = col0 + w + kstride * k;
+            if (MODE == 0) {
+                const double2* y1 = Y + (size_t)ti.vec * 2 * n;
+                cp_async16(dst + q, y1 + g);
+                cp_async16(dst + TE + q, y1 + n + g);
+            } else {
+                const double2* r1 = Y + (size_t)ti.vec * 2 * n;
+                const double2* p1 = Pcg + (size_t)ti.vec * 2 * n;
+                cp_async16(dst + q, r1 + g);
+                cp_async16(dst + TE + q, r1 + n + g);
+                cp_async16(dst + 2 * TE + q, p1 + g);
+                cp_async16(dst + 3 * TE + q, p1 + n + g);
+            }
+        }
+    };
+
+    int tile = blockIdx.x;
+    if (tile < ntiles) issue(tile, 0);
+    cp_async_commit();
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int nxt = tile + gridDim.x;
+        if (nxt < ntiles) issue(nxt, (it + 1) & 1);
+        cp_async_commit();
+        const TileIdx ti = tile_of(tile, nit, n2);
+        col_setup<W>(p, ti, cs);
+        cp_async_wait1();
+        __syncthreads();
+        const double2* sg = stage + (size_t)(it & 1) * NA * TE;
+        const int w = tid % W;
+        const ColS& c = cs[w];
+        const size_t gcol = (size_t)ti.i0 * W + w + (size_t)n1 * ti.j;
+        // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
+        {
+            double alpha_prev = 0.0, beta = 0.0;
+            double2 xv[2 * S];
+            if (MODE == 1) {
+                alpha_prev = cg.alpha[ti.vec];
+                beta = cg.beta[ti.vec];
+                const double2* x1 = Xcg + (size_t)ti.vec * 2 * n + gcol;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int e = tid + s * NT;
+                    if (e < TE) {
+                        xv[2 * s] = x1[kstride * (e / W)];
+                        xv[2 * s + 1] = x1[n + kstride * (e / W)];
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int e = tid + s * NT;
+                if (e < TE) {
+                    const int k = e / W;
+                    double2 u1 = sg[e], u2 = sg[TE + e];
+                    if (MODE == 1) {
+                        const double2 q1 = sg[2 * TE + e], q2 = sg[3 * TE + e];
+                        xv[2 * s] = make_double2(fma(alpha_prev, q1.x, xv[2 * s].x), fma(alpha_prev, q1.y, xv[2 * s].y));
+                        xv[2 * s + 1] =
+                            make_double2(fma(alpha_prev, q2.x, xv[2 * s + 1].x), fma(alpha_prev, q2.y, xv[2 * s + 1].y));
+                        u1 = make_double2(fma(beta, q1.x, u1.x), fma(beta, q1.y, u1.y));   // p <- r + beta p
+                        u2 = make_double2(fma(beta, q2.x, u2.x), fma(beta, q2.y, u2.y));
+                        double2* p1 = Pcg + (size_t)ti.vec * 2 * n + gcol + kstride * k;
+                        p1[0] = u1;
+                        p1[n] = u2;
+                        double2* x1 = Xcg + (size_t)ti.vec * 2 * n + gcol + kstride * k;
+                        x1[0] = xv[2 * s];
+                        x1[n] = xv[2 * s + 1];
+                    }
+                    const double2 l2 = modes::lam3(p, c.cm, hroot[k]);
+                    Coef o;
+                    const long long idx = c.cm.idx0 + (long long)kstride * k;
+                    modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
+                    const double2 U1 = cscale(u1, o.f1), U2 = cscale(u2, o.f2);
+                    Ct[e] = modes::comb(o, 0, U1, U2);
+                    Ct[TE + e] = modes::comb(o, 1, U1, U2);
+                    Ct[2 * TE + e] = modes::comb(o, 2, U1, U2);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- phase B: z-DFT of component l over k, twiddle, store ----
+        {
+            const int l = tid / (W * N2), t = (tid / W) % N2;
+            double2* ct = Ct + (size_t)l * TE;
+            double2 v[N1];
+#pragma unroll
+            for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
+            __syncthreads();
+            fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
+            const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+            const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
+            const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
+            const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
+            double2* out = U + (size_t)ti.vec * 3 * n + (size_t)l * n + gcol;
+            double2 au = wt;
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u) {
+                double2 f = au;
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) {
+                    const int cc = t + N2 * u + N1 * k2;
+                    out[kstride * cc] = cmul(v[u * N2 + k2], f);
+                    f = cmul(f, wk);
+                }
+                au = cmul(au, wu);
+            }
+        }
+        __syncthreads();   // stage (it & 1), Ct and cs are free
+    }
+}
+
+// ------------------------------------------------------------------ zadj
+// MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
+template <int N1, int N2, int W, int MODE>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 1)
+    k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, int nvec, CGFuse cg) {
+    using C = ZCfg<N1, N2, W>;
+    constexpr int N = C::N, NT = C::NT, TE = C::TE, S = C::S;
+    constexpr int NA = MODE ? 5 : 3;   // staged arrays: U0 U1 U2 | r1 r2
+    extern __shared__ double2 sm[];
+    double2* stage = sm;                    // [2][NA][TE]
+    double2* hroot = sm + 2 * NA * TE;      // [N]
+    __shared__ ColS cs[W];
+    __shared__ double2 red[32];
+    __shared__ double acc[8];
+    const ModeP& p = a.mp;
+    const long long n = p.n;
+    const int n1 = p.n1, n2 = p.n2;
+    const int nit = n1 / W;
+    const int ntiles = nit * n2 * nvec;
+    const size_t kstride = (size_t)n1 * n2;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < N; k += NT) hroot[k] = __ldg(a.hroot_z + k);
+    if (MODE == 1 && tid < 8) acc[tid] = 0.0;
+
+    auto issue = [&](int tile, int st) {
+        const TileIdx ti = tile_of(tile, nit, n2);
+        const size_t col0 = (size_t)ti.i0 * W + (size_t)n1 * ti.j;
+        double2* dst = stage + (size_t)st * NA * TE;
+        const double2* u0 = U + (size_t)ti.vec * 3 * n;
+#pragma unroll 1
+        for (int q = tid; q < TE; q += NT) {
+            const int k = q / W, w = q - k * W;
+            const size_t g = col0 + w + kstride * k;
+            cp_async16(dst + q, u0 + g);
+            cp_async16(dst + TE + q, u0 + n + g);
+            cp_async16(dst + 2 * TE + q, u0 + 2 * n + g);
+            if (MODE == 1) {
+                const double2* r1 = OUT + (size_t)ti.vec * 2 * n;
+                cp_async16(dst + 3 * TE + q, r1 + g);
+                cp_async16(dst + 4 * TE + q, r1 + n + g);
+            }
+        }
+    };
+
+    int tile = blockIdx.x;
+    if (tile < ntiles) issue(tile, 0);
+    cp_async_commit();
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int nxt = tile + gridDim.x;
+        if (nxt < ntiles) issue(nxt, (it + 1) & 1);
+        cp_async_commit();
+        const TileIdx ti = tile_of(tile, nit, n2);
+        col_setup<W>(p, ti, cs);
+        cp_async_wait1();
+        __syncthreads();
+        double2* sg = stage + (size_t)(it & 1) * NA * TE;
+        const int w = tid % W;
+        const ColS& c = cs[w];
+        const size_t gcol = (size_t)ti.i0 * W + w + (size_t)n1 * ti.j;
+        // ---- phase B: conj twiddle, z-DFT (-) of component l over c ----
+        {
+            const int l = tid / (W * N2), t = (tid / W) % N2;
+            double2* ct = sg + (size_t)l * TE;
+            const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+            double2 f = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
+            const double2 wu = conj2(tw_at(a.tw, ((unsigned long long)N2 * N3) % nn));
+            double2 v[N1];
+#pragma unroll
+            for (int m = 0; m < N1; ++m) {
+                v[m] = cmul(ct[(N2 * m + t) * W + w], f);
+                f = cmul(f, wu);
+            }
+            __syncthreads();
+            fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) ct[(t + N2 * u + N1 * k2) * W + w] = v[u * N2 + k2];
+        }
+        __syncthreads();
+        // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
+        double rr = 0.0;
+        const double alpha = MODE == 1 ? cg.alpha[ti.vec] : 0.0;
+        double2* o1 = OUT + (size_t)ti.vec * 2 * n + gcol;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int e = tid + s * NT;
+            if (e < TE) {
+                const int k = e / W;
+                const double2 l2 = modes::lam3(p, c.cm, hroot[k]);
+                Coef o;
+                const long long idx = c.cm.idx0 + (long long)kstride * k;
+                modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
+                const double2 w0 = sg[e], w1 = sg[TE + e], w2 = sg[2 * TE + e];
+                double2 z1 = cadd3(cjm(o.num1[0], w0), cjm(o.num1[1], w1), cjm(o.num1[2], w2));
+                double2 z2 = cadd3(cmul(o.d[0], w0), cmul(o.d[1], w1), cmul(o.d[2], w2));
+                z1 = cscale(z1, o.f1);
+                z2 = cscale(z2, o.f2);
+                if (MODE == 1) {
+                    double2 r1 = sg[3 * TE + e], r2 = sg[4 * TE + e];
+                    r1 = make_double2(fma(-alpha, z1.x, r1.x), fma(-alpha, z1.y, r1.y));
+                    r2 = make_double2(fma(-alpha, z2.x, r2.x), fma(-alpha, z2.y, r2.y));
+                    o1[kstride * k] = r1;
+                    o1[n + kstride * k] = r2;
+                    rr += fma(r1.x, r1.x, fma(r1.y, r1.y, fma(r2.x, r2.x, r2.y * r2.y)));
+                } else {
+                    o1[kstride * k] = z1;
+                    o1[n + kstride * k] = z2;
+                }
+            }
+        }
+        if (MODE == 1) {
+            const double2 bs = block_sum(make_double2(rr, 0.0), red);
+            if (tid == 0) acc[ti.vec] += bs.x;
+        }
+        __syncthreads();   // stage (it & 1) and cs are free
+    }
+    if (MODE == 1) {
+        // per-CTA partials of (r, r) for every vector; the last CTA forms beta
+        const int nb = gridDim.x;
+        if (tid < nvec) cg.part_z[(size_t)tid * nb + blockIdx.x] = acc[tid];
+        __syncthreads();
+        if (cg_last_block(cg.counter + 1, gridDim.x, red)) cg_finish_beta(cg, nb, nvec, red);
+    }
+}
+
+// x += alpha p (the CG update deferred by one iteration, k_zfwd2<MODE 1>)
+__global__ void k_cg_xfinal(double2* __restrict__ X, const double2* __restrict__ P, const double* __restrict__ alpha,
+                            long long N) {
+    const int v = blockIdx.y;
+    const double al = alpha[v];
+    if (al == 0.0) return;
+    double2* x = X + (size_t)v * N;
+    const double2* pp = P + (size_t)v * N;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        const double2 q = pp[t];
+        const double2 xv = x[t];
+        x[t] = make_double2(fma(al, q.x, xv.x), fma(al, q.y, xv.y));
+    }
+}
+
+template <int N1, int N2, int W>
+struct ZLaunch {
+    using C = ZCfg<N1, N2, W>;
+    static size_t smem_fwd(int mode) { return (size_t)(2 * (mode ? 4 : 2) * C::TE + 3 * C::TE + C::N) * sizeof(double2); }
+    static size_t smem_adj(int mode) { return (size_t)(2 * (mode ? 5 : 3) * C::TE + C::N) * sizeof(double2); }
+    template <class K>
+    static int grid(K kern, size_t smem, int ntiles) {
+        static int per_sm = -1;
+        static int nsm = 0;
+        if (per_sm < 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, smem);
+            if (per_sm < 1) per_sm = 1;
+        }
+        return std::max(1, std::min(ntiles, nsm * per_sm));
+    }
+};
+
+}  // namespace
+
+bool zpass2_supported(const OpArgs& a) {
+    if (!a.fast || a.hroot_z == nullptr) return false;
+    switch (a.mp.n3) {
+        case 64: return a.mp.n1 % 16 == 0;
+        case 96: return a.mp.n1 % 8 == 0;
+        case 128: return a.mp.n1 % 8 == 0;
+        case 192: return a.mp.n1 % 4 == 0;
+        case 256: return a.mp.n1 % 4 == 0;
+        default: return false;
+    }
+}
+
+template <int N1, int N2, int W>
+static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, double2* P, double2* X,
+                           const CGFuse* cg, cudaStream_t st) {
+    using L = ZLaunch<N1, N2, W>;
+    const int mode = cg ? 1 : 0;
+    const size_t smem = L::smem_fwd(mode);
+    const int ntiles = (a.mp.n1 / W) * a.mp.n2 * nvec;
+    if (mode) {
+        auto kern = k_zfwd2<N1, N2, W, 1>;
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(Y, U, a, 1, nvec, P, X, *cg);
+    } else {
+        auto kern = k_zfwd2<N1, N2, W, 0>;
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(Y, U, a, op, nvec, nullptr, nullptr, CGFuse{});
+    }
+    return cudaGetLastError();
+}
+
+template <int N1, int N2, int W>
+static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,
+                           cudaStream_t st) {
+    using L = ZLaunch<N1, N2, W>;
+    const int mode = cg ? 1 : 0;
+    const size_t smem = L::smem_adj(mode);
+    const int ntiles = (a.mp.n1 / W) * a.mp.n2 * nvec;
+    if (mode) {
+        auto kern = k_zadj2<N1, N2, W, 1>;
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(U, OUT, a, 1, nvec, *cg);
+    } else {
+        auto kern = k_zadj2<N1, N2, W, 0>;
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(U, OUT, a, op, nvec, CGFuse{});
+    }
+    return cudaGetLastError();
+}
+
+// n3 -> (N1, N2, W)
+#define BNF_Z2_PLANS(X) X(64, 8, 8, 16) X(96, 24, 4, 8) X(128, 16, 8, 8) X(192, 24, 8, 4) X(256, 16, 16, 4)
+
+cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, double2* P, double2* X,
+                         const CGFuse* cg, cudaStream_t st) {
+    switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: return zfwd2_t<A, B, WW>(a, Y, U, nvec, op, P, X, cg, st);
+        BNF_Z2_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,
+                         cudaStream_t st) {
+    switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: return zadj2_t<A, B, WW>(a, U, OUT, nvec, op, cg, st);
+        BNF_Z2_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return cudaErrorNotSupported;
+    }
+}
+
+cudaError_t launch_cg_xfinal(double2* X, const double2* P, const double* alpha, long long N, int nvec,
+                             cudaStream_t st) {
+    long long g = (N + 255) / 256;
+    if (g > 148 * 4) g = 148 * 4;
+    k_cg_xfinal<<<dim3((unsigned)g, nvec), 256, 0, st>>>(X, P, alpha, N);
+    return cudaGetLastError();
+}
+
+}  // namespace bnf

@@ -56,7 +56,7 @@ def main():
                 t = kms / cnt
                 by = PASS_BYTES[k](n) * b if k in PASS_BYTES else 0
                 per[k] = {"us": round(1000 * t, 1), "GBps": round(by / (t / 1e3) / 1e9, 1) if by else None}
-            tot_bytes = sum(PASS_BYTES[k](n) for k in ("zfwd", "yfwd", "xpass", "yadj", "zadj")) * b
+            tot_bytes = sum(PASS_BYTES[k](n) for k in kt if k in PASS_BYTES) * b
             rec = {"config": cfg.name, "n": n, "b": b, "ms_per_apply": ms, "matvecs_per_s": b / (ms / 1e3),
                    "algorithmic_GBps": tot_bytes / (ms / 1e3) / 1e9, "frac_of_peak": tot_bytes / (ms / 1e3) / 1e9 / peak,
                    "passes": per}
