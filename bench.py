@@ -199,6 +199,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1806_10284_b200 as bnf
+    from paper_1806_10284_b200 import kpath
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -212,8 +213,10 @@ def main():
     S.set_epsilon(eps)
     nev = cfg.nev
 
+    share = kpath.assign(ks, world)[rank]   # LPT share of the path (no data-path collective)
+
     def kidx(step):
-        return (step * world + rank) % len(ks)
+        return share[step % len(share)]
 
     def barrier():
         if world > 1:

@@ -1,0 +1,118 @@
+"""Host logic of the k-path scheduler (paper_1806_10284_b200/kpath.py):
+assignment, retry/checkpoint, and the multi-process gather over gloo
+(world_size 2, CPU) -- the N > 1 path of bench.py / solve_path without a GPU."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1806_10284_b200 import kpath  # noqa: E402
+from synthetic import configs  # noqa: E402
+
+
+def _fake_solve(kap):
+    # deterministic stand-in for Solver.solve: lambda depends only on kappa
+    k = np.asarray(kap)
+    lam = np.sort(np.abs(np.sin(np.arange(1, 5) * (1.0 + k.sum()))) + 0.1)
+    return lam.tolist(), {"rc": 0, "matvecs": 10}
+
+
+def _path():
+    return [tuple(x) for x in configs.config(4).kappa_direct]
+
+
+def test_assign_covers_every_k_once_and_balances():
+    kaps = _path()
+    for world in (1, 2, 3, 8):
+        share = kpath.assign(kaps, world)
+        flat = sorted(i for s in share for i in s)
+        assert flat == list(range(len(kaps)))
+        costs = [kpath.kpoint_cost(k) for k in kaps]
+        loads = [sum(costs[i] for i in s) for s in share]
+        assert max(loads) - min(loads) <= max(costs) + 1e-12
+        assert share == kpath.assign(kaps, world)   # deterministic
+
+
+def test_gamma_is_costlier():
+    assert kpath.kpoint_cost((0.0, 0.0, 0.0)) > kpath.kpoint_cost((0.1, 0.2, 0.3))
+    assert kpath.kpoint_cost((0.5, 0.0, 0.5)) > kpath.kpoint_cost((0.4, 0.1, 0.3))
+
+
+def test_retry_and_failure_recorded():
+    calls = {"n": 0}
+
+    def flaky(kap):
+        calls["n"] += 1
+        if kap[0] == 0.0 and calls["n"] == 1:
+            raise RuntimeError("transient")
+        if kap[0] < 0:
+            raise RuntimeError("always")
+        return _fake_solve(kap)
+
+    kaps = [(0.0, 0.0, 0.0), (-1.0, 0.0, 0.0), (0.2, 0.1, 0.0)]
+    recs = kpath.run_path(flaky, kaps, [0, 1, 2], retries=1)
+    assert [r.status for r in recs] == ["ok", "failed", "ok"]
+    assert recs[0].attempts == 2 and recs[1].attempts == 2
+
+
+def test_checkpoint_resume_skips_finished(tmp_path):
+    kaps = _path()[:6]
+    ck = str(tmp_path / "rank0.jsonl")
+    first = kpath.run_path(_fake_solve, kaps, [0, 1, 2], checkpoint=ck)
+    with open(ck, "a") as f:
+        f.write('{"index": 3, "kappa": [')   # torn line of an interrupted run
+    seen = []
+
+    def counting(kap):
+        seen.append(kap)
+        return _fake_solve(kap)
+
+    second = kpath.run_path(counting, kaps, list(range(6)), checkpoint=ck)
+    assert len(seen) == 3                                     # only k = 3, 4, 5 solved again
+    assert [r.lam for r in second[:3]] == [r.lam for r in first]
+    assert [r.index for r in second] == list(range(6))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kaps = _path()
+    share = kpath.assign(kaps, world)[rank]
+    recs = kpath.run_path(_fake_solve, kaps, share, rank=rank)
+    merged = kpath.gather(recs, len(kaps))
+    if rank == 0:
+        with open(os.path.join(out_dir, "merged.json"), "w") as f:
+            json.dump([[r.index, r.rank, r.lam] for r in merged], f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_world2_gloo_equals_single_process(tmp_path):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    with open(tmp_path / "merged.json") as f:
+        merged = json.load(f)
+    kaps = _path()
+    single = kpath.merge([kpath.run_path(_fake_solve, kaps, range(len(kaps)))], len(kaps))
+    assert [m[0] for m in merged] == list(range(len(kaps)))
+    assert {m[1] for m in merged} == {0, 1}                    # both ranks contributed
+    for m, s in zip(merged, single):
+        assert m[2] == s.lam
+
+
+def test_frequencies_convention():
+    lam = [4 * np.pi ** 2, 0.0]
+    assert kpath.frequencies(lam) == [1.0, 0.0]
