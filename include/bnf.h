@@ -169,6 +169,13 @@ int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem);
 int bnf_kernel_times(bnf_solver* s, const char** names, double* ms, long long* launches, int cap, int* count);
 int bnf_kernel_times_reset(bnf_solver* s);
 
+/* Switch per-kernel timing on (1) or off (0) after creation (opts.profile).
+   With profiling on, the CG loop runs eagerly with one CUDA-event pair per
+   kernel and a host convergence check per iteration; with it off the CG loop
+   is one CUDA graph with a device-side while condition (no host round trip
+   per iteration).  Both paths execute the same kernels on the same data. */
+int bnf_set_profile(bnf_solver* s, int on);
+
 const char* bnf_last_error(void);
 int bnf_version(void);
 

@@ -72,6 +72,7 @@ _sigs = {
     "bnf_kernel_times": [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int,
                          C.POINTER(C.c_int)],
     "bnf_kernel_times_reset": [_P],
+    "bnf_set_profile": [_P, C.c_int],
     "bnf_host_herm_eig": [C.c_int, _P, _P, _P],
 }
 for _name, _args in _sigs.items():
@@ -86,7 +87,7 @@ _lib.bnf_opts_default.restype = None
 
 EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce",
            "bnf_opts_default", "bnf_solver_create", "bnf_solver_destroy", "bnf_set_epsilon", "bnf_set_kappa",
-           "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset",
+           "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile",
            "bnf_last_error", "bnf_version", "bnf_host_herm_eig"]
 
 
@@ -205,6 +206,10 @@ class Solver:
         if reset:
             _check(_lib.bnf_kernel_times_reset(self._h))
         return out
+
+    def set_profile(self, on):
+        """Per-kernel CUDA-event timing on/off (off: CG loop as one CUDA graph)."""
+        _check(_lib.bnf_set_profile(self._h, int(bool(on))))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -19,7 +19,20 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
 }
 
 // block-wide sum of one complex value (blockDim.x multiple of 32, <= 1024)
+// red: >= 32 entries, or >= blockDim.x entries when blockDim.x is not a
+// multiple of 32 (a partial warp cannot use full-mask shuffles; the sum is
+// then taken serially, still in a fixed order).
 __device__ double2 block_sum(double2 v, double2* red) {
+    if (blockDim.x & 31u) {
+        __syncthreads();
+        red[threadIdx.x] = v;
+        __syncthreads();
+        double2 r = make_double2(0, 0);
+        if (threadIdx.x == 0)
+            for (unsigned t = 0; t < blockDim.x; ++t) r = make_double2(r.x + red[t].x, r.y + red[t].y);
+        __syncthreads();
+        return r;  // valid in thread 0
+    }
     v = warp_sum(v);
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     __syncthreads();
@@ -83,7 +96,19 @@ __device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scra
             cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;
         }
     }
-    if (threadIdx.x == 0) cg.counter[1] = 0u;
+    if (threadIdx.x == 0) {
+        cg.counter[1] = 0u;
+        // device-side loop control of the CG graph (solver.cu, cg_graph): continue
+        // while any vector is active and the iteration cap is not reached
+        if (cg.iter != nullptr) {
+            int any = 0;
+            for (int v = 0; v < nvec; ++v) any |= cg.active[v];
+            const int it = ++cg.iter[0];
+            cg.iter[1] += 1;
+            cg.iter[2] += nvec;
+            if (cg.use_cond) cudaGraphSetConditional(cg.cond, (any && it < cg.max_iter) ? 1u : 0u);
+        }
+    }
 }
 
 }  // namespace

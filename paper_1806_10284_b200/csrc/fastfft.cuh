@@ -97,20 +97,56 @@ __host__ __device__ constexpr int first_factor(int n) {
 }
 
 template <int N, int S>
+struct DFT;
+
+// v * w_N^{S J} with J a compile-time constant: the twiddle is a literal
+// (trivial ones -- 1, -1, +-i -- cost no multiplications)
+template <int N, int S, int J>
+__device__ __forceinline__ double2 twc(double2 a) {
+    constexpr int jj = ((J % N) + N) % N;
+    if constexpr (jj == 0) {
+        return a;
+    } else if constexpr (4 * jj == N) {
+        return mul_i<S>(a);
+    } else if constexpr (2 * jj == N) {
+        return make_double2(-a.x, -a.y);
+    } else if constexpr (4 * jj == 3 * N) {
+        return mul_i<-S>(a);
+    } else {
+        constexpr double c = trig2pi(jj, N, false);
+        constexpr double sn = S > 0 ? trig2pi(jj, N, true) : -trig2pi(jj, N, true);
+        return make_double2(a.x * c - a.y * sn, a.x * sn + a.y * c);
+    }
+}
+
+template <int N, int S, int A, int b, int k1>
+__device__ __forceinline__ void tw_row(const double2* t, double2* y) {
+    if constexpr (k1 < A) {
+        y[b * A + k1] = twc<N, S, b * k1>(t[k1]);
+        tw_row<N, S, A, b, k1 + 1>(t, y);
+    }
+}
+
+template <int N, int S, int A, int B, int b>
+__device__ __forceinline__ void dft_cols(const double2* v, double2* y) {
+    if constexpr (b < B) {
+        double2 t[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) t[a] = v[B * a + b];
+        DFT<A, S>::run(t);
+        tw_row<N, S, A, b, 0>(t, y);
+        dft_cols<N, S, A, B, b + 1>(v, y);
+    }
+}
+
+// Mixed-radix N = A * B register DFT (Cooley-Tukey, compile-time twiddles)
+template <int N, int S>
 struct DFT {
     static __device__ __forceinline__ void run(double2* v) {
         constexpr int A = first_factor(N);
         constexpr int B = N / A;
         double2 y[N];
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            double2 t[A];
-#pragma unroll
-            for (int a = 0; a < A; ++a) t[a] = v[B * a + b];
-            DFT<A, S>::run(t);
-#pragma unroll
-            for (int k1 = 0; k1 < A; ++k1) y[b * A + k1] = (b * k1 == 0) ? t[k1] : cmul(t[k1], ctw<N, S>(b * k1));
-        }
+        dft_cols<N, S, A, B, 0>(v, y);
 #pragma unroll
         for (int k1 = 0; k1 < A; ++k1) {
             double2 t[B];

@@ -72,6 +72,10 @@ struct CGFuse {
     double* beta;
     double* thr;
     int* active;
+    int* iter;                         // CG iterations done (device), or null
+    int max_iter;
+    int use_cond;                      // 1: set the CG graph's while-condition
+    cudaGraphConditionalHandle cond;
 };
 
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()

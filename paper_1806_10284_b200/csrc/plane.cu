@@ -38,15 +38,42 @@ __device__ __forceinline__ double2 tw_at(const TwP& t, unsigned long long P) {  
 }
 __device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
 template <int P>
 struct Cluster {
     __device__ static unsigned rank() { return P == 1 ? 0u : cgx::this_cluster().block_rank(); }
+    // full barrier with release/acquire: remote stores before it are visible after it
     __device__ static void sync() {
-        if (P == 1) __syncthreads();
-        else cgx::this_cluster().sync();
+        if (P == 1) {
+            __syncthreads();
+        } else {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        }
     }
-    __device__ static double2* map(double2* p, unsigned r) {
-        return P == 1 ? p : cgx::this_cluster().map_shared_rank(p, r);
+    // barrier only ("every CTA has consumed its D"): the reads it orders have
+    // already completed (their values were used), so no fence is needed
+    __device__ static void sync_relaxed() {
+        if (P == 1) {
+            __syncthreads();
+        } else {
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+        }
+    }
+    // store v to element e of CTA r's copy of the shared array at byte address base
+    __device__ static void put(double2* local, unsigned base, unsigned r, int e, double2 v) {
+        if (P == 1) {
+            local[e] = v;
+        } else {
+            unsigned ra;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(base + 16u * (unsigned)e), "r"(r));
+            asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(ra), "d"(v.x), "d"(v.y) : "memory");
+        }
     }
 };
 
@@ -64,7 +91,6 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
     extern __shared__ double2 D[];
-    __shared__ double2 red[32];
     const ModeP& p = a.mp;
     const unsigned r = Cluster<P>::rank();
     const int c = blockIdx.x / P;
@@ -73,6 +99,15 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const int tid = threadIdx.x;
     double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
     double2 v[N1];
+    // B^{-1} material indices of this CTA's phase-X rows (contiguous CW*N bytes), prefetched
+    constexpr bool EPF = (N % 16) == 0;
+    unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);
+    const bool epf = EPF && a.eps_idx != nullptr;
+    if (epf) {
+        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * ((size_t)r * CW + (size_t)N * c);
+        for (int q = threadIdx.x; q < CW * N / 16; q += C::NT) cp_async16(eps_s + 16 * q, src + 16 * q);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
 
     // ---------------- phase Y: columns i = r*CW + w, FFT over j ----------------
     const int w = tid % CW, t = tid / CW;
@@ -105,15 +140,16 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         }
     }
     // exchange Y -> X: element (b, i) goes to CTA b / CW, row b % CW, column i
-    Cluster<P>::sync();   // every CTA is done with its own D
+    const unsigned dbase = (unsigned)__cvta_generic_to_shared(D);
+    Cluster<P>::sync_relaxed();   // every CTA is done with its own D
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
             const int b = t + N2 * u + N1 * k2;
-            double2* dst = Cluster<P>::map(D, (unsigned)(b / CW));
-            dst[(b % CW) * N + i] = v[u * N2 + k2];
+            Cluster<P>::put(D, dbase, (unsigned)(b / CW), (b % CW) * N + i, v[u * N2 + k2]);
         }
+    if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     Cluster<P>::sync();
 
     // ---------------- phase X: rows b = r*CW + rw, FFT over i ----------------
@@ -131,8 +167,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
                 const int aa = tx + N2 * u + N1 * k2;
-                const double e_ = a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
-                                            : __ldg(a.eps_inv + rowofs + aa);
+                const double e_ = epf ? __ldg(a.eps_lut + eps_s[rw * N + aa])
+                                      : (a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
+                                                   : __ldg(a.eps_inv + rowofs + aa));
                 const double s_ = a.inv_n * e_;
                 const double2 x = v[u * N2 + k2];
                 if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
@@ -144,17 +181,18 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
-        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, red);
-        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, red)) cg_finish_alpha(cgf, nb, nvec_all, red);
+        // D is free here (between the x-FFTs) and holds >= blockDim entries
+        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D)) cg_finish_alpha(cgf, nb, nvec_all, D);
+        __syncthreads();
     }
     fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
     // exchange X -> Y: element (b, a) goes to CTA a / CW, row b, column a % CW (ld CW)
-    Cluster<P>::sync();
+    Cluster<P>::sync_relaxed();
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
         const int aa = N2 * m + tx;
-        double2* dst = Cluster<P>::map(D, (unsigned)(aa / CW));
-        dst[b * CW + (aa % CW)] = v[m];
+        Cluster<P>::put(D, dbase, (unsigned)(aa / CW), b * CW + (aa % CW), v[m]);
     }
     Cluster<P>::sync();
 
@@ -185,7 +223,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 template <int N1, int N2, int P>
 cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
-    const size_t smem = (size_t)C::SMEM * sizeof(double2);
+    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (size_t)C::CW * C::N;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(P * a.mp.n3), (unsigned)nslab, 1);
     cfg.blockDim = dim3(C::NT, 1, 1);

@@ -187,7 +187,22 @@ struct bnf_solver {
     bool fused_ok = false;
     bool l2_slabs = false;
     bool use_plane = false;   // fused y/x/y plane pass (plane.cu)
-    bool use_z2 = false;      // persistent pipelined z passes (zpass.cu)
+    bool use_z2 = false;      // cp.async-staged z passes (zpass.cu)
+    bool use_graph = true;    // CG loop as a CUDA graph with a device-side while node
+    struct CgGraph {
+        cudaGraphExec_t exec = nullptr;
+        const void* X = nullptr;
+        int nvec = 0;
+        long long kver = -1;
+        int nk = 0;
+    } cgg[2];
+    int cgg_next = 0;
+    cudaStream_t cap = nullptr;   // capture stream
+    long long kver = 0;           // bumped whenever OpArgs change (kappa, eps)
+    DevBuf iterbuf;               // int[3]: per-call CG iterations, total iterations, total vector-iterations
+    int* d_iter = nullptr;
+    int graph_kernels_per_iter = 0;
+    long long graph_calls = 0;
     DevBuf hroot;             // e^{i pi k / n3}
     DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
@@ -201,6 +216,9 @@ struct bnf_solver {
     long long inner_iters = 0;
 
     ~bnf_solver() {
+        for (auto& c : cgg)
+            if (c.exec) cudaGraphExecDestroy(c.exec);
+        if (cap) cudaStreamDestroy(cap);
         if (h_flags) cudaFreeHost(h_flags);
         if (h_small) cudaFreeHost(h_small);
     }
@@ -337,9 +355,97 @@ int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_o
     return BNF_OK;
 }
 
+// One CG iteration of cg_solve_fused on stream st (eager or under capture).
+// Returns the number of kernels enqueued in *nk.
+cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2* P, double2* U, double2* X, int nvec,
+                            cudaStream_t st, int* nk) {
+    cudaError_t e;
+    int k = 0;
+#define BNF_K(expr)                       \
+    do {                                  \
+        e = (expr);                       \
+        if (e != cudaSuccess) return e;   \
+        ++k;                              \
+    } while (0)
+    if (s->use_z2) BNF_K(launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, st));
+    else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
+    if (s->use_plane) {
+        BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
+    } else {
+        BNF_K(launch_ypass(s->args, U, nvec, 0, st));
+        BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
+        BNF_K(launch_ypass(s->args, U, nvec, 1, st));
+    }
+    if (s->use_z2) BNF_K(launch_zadj2(s->args, U, R, nvec, 1, &cg, st));
+    else BNF_K(launch_zadj_cg(s->args, U, X, nvec, cg, st));
+#undef BNF_K
+    *nk = k;
+    return cudaSuccess;
+}
+
+// CUDA graph of the whole CG loop: a device-side WHILE node whose body is one
+// CG iteration; the last CTA of the zadj pass sets the condition (any vector
+// still active and iterations < max_inner, cgfuse.cuh).  No host round trip
+// per iteration.  Cached per (output block, nvec, operator version).
+int cg_graph(bnf_solver* s, const CGFuse& cg0, double2* R, double2* P, double2* U, double2* X, int nvec,
+             cudaGraphExec_t* out, int* nk) {
+    for (auto& c : s->cgg)
+        if (c.exec && c.X == X && c.nvec == nvec && c.kver == s->kver) {
+            *out = c.exec;
+            *nk = c.nk;
+            return BNF_OK;
+        }
+    if (!s->cap) CK(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    CGFuse cg = cg0;
+    cg.use_cond = 1;
+    cg.cond = h;
+    CK(cudaStreamBeginCaptureToGraph(s->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    int k = 0;
+    cudaError_t e = cg_iter_kernels(s, cg, R, P, U, X, nvec, s->cap, &k);
+    cudaGraph_t captured = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(s->cap, &captured);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+        cudaGraphDestroy(g);
+        set_error(std::string("CG graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+        return BNF_ECUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        set_error(std::string("CG graph instantiate: ") + cudaGetErrorString(e));
+        return BNF_ECUDA;
+    }
+    auto& slot = s->cgg[s->cgg_next];
+    s->cgg_next = (s->cgg_next + 1) % 2;
+    if (slot.exec) cudaGraphExecDestroy(slot.exec);
+    slot.exec = exec;
+    slot.X = X;
+    slot.nvec = nvec;
+    slot.kver = s->kver;
+    slot.nk = k;
+    *out = exec;
+    *nk = k;
+    return BNF_OK;
+}
+
 // Same CG with the vector updates and reductions fused into the operator
-// passes (kernels.cu: zfwd p-update, x-pass (p,Mp)/alpha, zadj x/r update,
-// (r,r)/beta).  Used when every axis has a register-FFT plan.
+// passes (zfwd: x += alpha_prev p, p <- r + beta p; plane/x pass: (p, M p)
+// and alpha; zadj: r -= alpha M p, (r, r) and beta).  Used when every axis
+// has a register-FFT plan.  Without profiling the loop runs as one CUDA
+// graph with a device-side while condition.
 int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
     const long long N = 2 * s->n;
     const size_t vb = (size_t)N * nvec * sizeof(double2);
@@ -361,41 +467,45 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     cg.P = P;
     cg.R = R;
     int it = 0;
-    for (; it < s->o.max_inner; ++it) {
-        if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
-        else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
-        if (s->use_plane) {
-            RUN("plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
-        } else if (s->l2_slabs) {
-            // y -> x -> y per component slab: the slab stays resident in L2 between the passes
-            OpArgs sa = s->args;
-            sa.nvec_all = nvec;
-            for (int vl = 0; vl < 3 * nvec; ++vl) {
-                sa.comp0 = vl;
-                RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
-                RUN("xpass_cg", launch_xpass_slab(sa, U, &cg, s->st));
-                RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
+    if (!s->prof.on && s->use_graph) {
+        cg.iter = s->d_iter;
+        cg.max_iter = s->o.max_inner;
+        CK(cudaMemsetAsync(s->d_iter, 0, sizeof(int), s->st));   // per-call counter; [1], [2] run on
+        cudaGraphExec_t exec = nullptr;
+        int nk = 0;
+        TRY(cg_graph(s, cg, R, P, U, X, nvec, &exec, &nk));
+        CK(cudaGraphLaunch(exec, s->st));
+        s->graph_kernels_per_iter = nk;
+        s->graph_calls++;
+    } else {
+        cg.iter = nullptr;
+        for (; it < s->o.max_inner; ++it) {
+            // eager: one timed launch per pass (profiling, bnf_kernel_times)
+            if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
+            else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
+            if (s->use_plane) {
+                RUN("plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+            } else {
+                RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
+                RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
+                RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
             }
-        } else {
-            RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
-            RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
-            RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
+            if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
+            else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
+            s->matvecs += nvec;
+            CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
+            CK(cudaStreamSynchronize(s->st));
+            if (s->prof.on) s->prof.flush();
+            int act = 0;
+            for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
+            if (act == 0) {
+                ++it;
+                break;
+            }
         }
-        if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
-        else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
-        s->matvecs += nvec;
-        CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
-        CK(cudaStreamSynchronize(s->st));
-        if (s->prof.on) s->prof.flush();
-        int act = 0;
-        for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
-        if (act == 0) {
-            ++it;
-            break;
-        }
+        s->inner_iters += (long long)it * nvec;
     }
     if (s->use_z2) RUN("cg_xfinal", launch_cg_xfinal(X, P, s->cgf.alpha, N, nvec, s->st));
-    s->inner_iters += (long long)it * nvec;
     if (iters_out) *iters_out = it;
     return BNF_OK;
 }
@@ -543,6 +653,7 @@ int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
     }
     RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st));
     s->kappa_set = true;
+    s->kver++;
     return BNF_OK;
 }
 
@@ -741,6 +852,10 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         s->args.hroot_z = s->hroot.as<double2>();
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
+    s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
+    CK(s->iterbuf.ensure(4 * sizeof(int)));
+    CK(cudaMemset(s->iterbuf.p, 0, 4 * sizeof(int)));
+    s->d_iter = s->iterbuf.as<int>();
     if (s->fused_ok) {
         const size_t per = cg_partials_per_vec(s->args);
         const size_t bytes = 2 * 8 * per * sizeof(double) + 4 * 64 * sizeof(double) + 64;
@@ -821,6 +936,7 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
     }
     CK(cudaStreamSynchronize(s->st));
     s->eps_set = true;
+    s->kver++;
     return BNF_OK;
 }
 
@@ -862,6 +978,8 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     const long long launches0 = s->prof.launches;
     s->matvecs = 0;
     s->inner_iters = 0;
+    s->graph_calls = 0;
+    CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
     TRY(set_kappa_impl(s, kappa));
     const long long N = 2 * s->n;
     const int b = s->o.block;
@@ -1046,12 +1164,20 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     for (int c = 0; c < nev; ++c) lambda[c] = lam[c];
     CK(cudaStreamSynchronize(s->st));
     if (s->prof.on) s->prof.flush();
+    long long graph_launches = 0;
+    if (s->graph_calls > 0) {   // CG iterations run inside graphs were counted on the device
+        int h[3];
+        CK(cudaMemcpy(h, s->d_iter, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+        s->inner_iters += h[2];
+        s->matvecs += h[2];
+        graph_launches = (long long)h[1] * s->graph_kernels_per_iter;
+    }
     if (stats) {
         stats->outer_steps = m;
         stats->converged = converged ? 1 : 0;
         stats->inner_iters = s->inner_iters;
         stats->matvecs = s->matvecs;
-        stats->kernel_launches = s->prof.launches - launches0;
+        stats->kernel_launches = s->prof.launches - launches0 + graph_launches;
         stats->max_ritz_residual = maxres;
         stats->max_residual = maxr_ar;
         stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1122,6 +1248,18 @@ int bnf_kernel_times(bnf_solver* s, const char** names, double* ms, long long* l
         ++k;
     }
     *count = k;
+    return BNF_OK;
+}
+
+int bnf_set_profile(bnf_solver* s, int on) {
+    if (!s) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    CK(cudaStreamSynchronize(s->st));
+    if (s->prof.on) s->prof.flush();
+    s->prof.on = on != 0;
+    s->o.profile = on != 0;
     return BNF_OK;
 }
 

@@ -1,15 +1,15 @@
-// Fourier-side z passes of the null-space-free matvec, persistent and
-// software-pipelined (§5.3):
+// Fourier-side z passes of the null-space-free matvec (SURVEY.md §8(a)
+// a1-a2 and a4-a5; §5.3):
 //
 //   zfwd : Sigma_r, Pi combine (2 -> 3 components), z-DFT k -> c (+),
 //          twiddle e^{+2 pi i c N3(i,j)/n}                       (Alg. 2 step 1)
 //   zadj : conj twiddle, z-DFT c -> k (-), Pi^* combine (3 -> 2), Sigma_r
 //                                                                (Alg. 1 step 3)
 //
-// One CTA per SM loops over column tiles (W consecutive i, one j, all k).
-// The next tile's inputs stream into a second shared-memory stage with
-// cp.async while the current tile is computed, so HBM stays busy through
-// the FP64 mode algebra and the register FFTs.  Inter-axis twiddles are
+// One CTA per column tile (W consecutive i, one j, all k); the whole tile is
+// fetched with cp.async at once and two CTAs per SM overlap one tile's HBM
+// traffic with the other's FP64 mode algebra and register FFTs.  Inter-axis
+// twiddles are
 // products of three exact table entries (no per-element table gathers);
 // lambda3 along k comes from the column's half angle and an exact
 // e^{i pi k/n3} table (modes.cuh).
@@ -41,7 +41,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ double2 tw_at(const TwP& t, unsigned long long P) {  // e^{2 pi i P / n}
     return cmul(__ldg(t.hi + (P >> t.shift)), __ldg(t.lo + (P & t.mask)));
@@ -67,292 +67,210 @@ struct ColS {   // per-column constants shared through smem
     unsigned long long base3;   // N3(i, j) mod n
 };
 
-struct TileIdx {
-    int i0, j, vec;
-};
-__device__ __forceinline__ TileIdx tile_of(int tile, int nit, int n2) {
-    TileIdx t;
-    t.i0 = (tile % nit);
-    const int r = tile / nit;
-    t.j = r % n2;
-    t.vec = r / n2;
-    return t;
-}
-
-template <int W>
-__device__ __forceinline__ void col_setup(const ModeP& p, const TileIdx& ti, ColS* cs) {
-    if (threadIdx.x < W) {
-        const int i = ti.i0 * W + threadIdx.x;
-        cs[threadIdx.x].cm = modes::col(p, i, ti.j);
-        cs[threadIdx.x].base3 =
-            (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)ti.j) % p.n);
-    }
-}
-
 // ------------------------------------------------------------------ zfwd
-// MODE 0: U = Q_r Sigma_op Y (op = a runtime 0 A_r / 1 M).  MODE 1: CG (op M).
+// One CTA per column tile (W consecutive i, one j, all k, one vector).  All
+// tile inputs are issued at once with cp.async (no register cost), so two
+// CTAs per SM overlap one tile's loads with the other's FP64 work.  The
+// three component tiles of the FFT phase alias the consumed input stage.
+// MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 1)
-    k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, int nvec, double2* __restrict__ Pcg,
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
+    k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
-    constexpr int N = C::N, NT = C::NT, TE = C::TE, S = C::S;
-    constexpr int NA = MODE ? 4 : 2;   // staged arrays: y1 y2 | r1 r2 p1 p2
-    extern __shared__ double2 sm[];
-    double2* stage = sm;                       // [2][NA][TE]
-    double2* Ct = sm + 2 * NA * TE;            // [3][TE] component tiles
-    double2* hroot = Ct + 3 * TE;              // [N]
+    constexpr int NT = C::NT, TE = C::TE;
+    extern __shared__ double2 sm[];   // [NA][TE]: y1 y2 (+1) | r1 r2 p1 p2 x1 x2; Ct = [0..3)
     __shared__ ColS cs[W];
     const ModeP& p = a.mp;
     const long long n = p.n;
-    const int n1 = p.n1, n2 = p.n2;
-    const int nit = n1 / W;
-    const int ntiles = nit * n2 * nvec;
-    const size_t kstride = (size_t)n1 * n2;
+    const int n1 = p.n1;
+    const size_t kstride = (size_t)n1 * p.n2;
     const int tid = threadIdx.x;
-    for (int k = tid; k < N; k += NT) hroot[k] = __ldg(a.hroot_z + k);
-
-    auto issue = [&](int tile, int st) {
-        const TileIdx ti = tile_of(tile, nit, n2);
-        const size_t col0 = (size_t)ti.i0 * W + (size_t)n1 * ti.j;
-        double2* dst = stage + (size_t)st * NA * TE;
-#pragma unroll 1
+    const int i0 = blockIdx.x * W, j = blockIdx.y, vec = blockIdx.z;
+    const size_t col0 = (size_t)i0 + (size_t)n1 * j;
+    {
+        const double2* y1 = Y + (size_t)vec * 2 * n + col0;
+        const double2* p1 = MODE ? Pcg + (size_t)vec * 2 * n + col0 : nullptr;
+        const double2* x1 = MODE ? Xcg + (size_t)vec * 2 * n + col0 : nullptr;
+#pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
-            const int k = q / W, w = q - k * W;
-            const size_t g = col0 + w + kstride * k;
-            if (MODE == 0) {
-                const double2* y1 = Y + (size_t)ti.vec * 2 * n;
-                cp_async16(dst + q, y1 + g);
-                cp_async16(dst + TE + q, y1 + n + g);
-            } else {
-                const double2* r1 = Y + (size_t)ti.vec * 2 * n;
-                const double2* p1 = Pcg + (size_t)ti.vec * 2 * n;
-                cp_async16(dst + q, r1 + g);
-                cp_async16(dst + TE + q, r1 + n + g);
-                cp_async16(dst + 2 * TE + q, p1 + g);
-                cp_async16(dst + 3 * TE + q, p1 + n + g);
-            }
-        }
-    };
-
-    int tile = blockIdx.x;
-    if (tile < ntiles) issue(tile, 0);
-    cp_async_commit();
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-        const int nxt = tile + gridDim.x;
-        if (nxt < ntiles) issue(nxt, (it + 1) & 1);
-        cp_async_commit();
-        const TileIdx ti = tile_of(tile, nit, n2);
-        col_setup<W>(p, ti, cs);
-        cp_async_wait1();
-        __syncthreads();
-        const double2* sg = stage + (size_t)(it & 1) * NA * TE;
-        const int w = tid % W;
-        const ColS& c = cs[w];
-        const size_t gcol = (size_t)ti.i0 * W + w + (size_t)n1 * ti.j;
-        // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
-        {
-            double alpha_prev = 0.0, beta = 0.0;
-            double2 xv[2 * S];
+            const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
+            cp_async16(sm + q, y1 + g);
+            cp_async16(sm + TE + q, y1 + n + g);
             if (MODE == 1) {
-                alpha_prev = cg.alpha[ti.vec];
-                beta = cg.beta[ti.vec];
-                const double2* x1 = Xcg + (size_t)ti.vec * 2 * n + gcol;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const int e = tid + s * NT;
-                    if (e < TE) {
-                        xv[2 * s] = x1[kstride * (e / W)];
-                        xv[2 * s + 1] = x1[n + kstride * (e / W)];
-                    }
-                }
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int e = tid + s * NT;
-                if (e < TE) {
-                    const int k = e / W;
-                    double2 u1 = sg[e], u2 = sg[TE + e];
-                    if (MODE == 1) {
-                        const double2 q1 = sg[2 * TE + e], q2 = sg[3 * TE + e];
-                        xv[2 * s] = make_double2(fma(alpha_prev, q1.x, xv[2 * s].x), fma(alpha_prev, q1.y, xv[2 * s].y));
-                        xv[2 * s + 1] =
-                            make_double2(fma(alpha_prev, q2.x, xv[2 * s + 1].x), fma(alpha_prev, q2.y, xv[2 * s + 1].y));
-                        u1 = make_double2(fma(beta, q1.x, u1.x), fma(beta, q1.y, u1.y));   // p <- r + beta p
-                        u2 = make_double2(fma(beta, q2.x, u2.x), fma(beta, q2.y, u2.y));
-                        double2* p1 = Pcg + (size_t)ti.vec * 2 * n + gcol + kstride * k;
-                        p1[0] = u1;
-                        p1[n] = u2;
-                        double2* x1 = Xcg + (size_t)ti.vec * 2 * n + gcol + kstride * k;
-                        x1[0] = xv[2 * s];
-                        x1[n] = xv[2 * s + 1];
-                    }
-                    const double2 l2 = modes::lam3(p, c.cm, hroot[k]);
-                    Coef o;
-                    const long long idx = c.cm.idx0 + (long long)kstride * k;
-                    modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
-                    const double2 U1 = cscale(u1, o.f1), U2 = cscale(u2, o.f2);
-                    Ct[e] = modes::comb(o, 0, U1, U2);
-                    Ct[TE + e] = modes::comb(o, 1, U1, U2);
-                    Ct[2 * TE + e] = modes::comb(o, 2, U1, U2);
-                }
+                cp_async16(sm + 2 * TE + q, p1 + g);
+                cp_async16(sm + 3 * TE + q, p1 + n + g);
+                cp_async16(sm + 4 * TE + q, x1 + g);
+                cp_async16(sm + 5 * TE + q, x1 + n + g);
             }
         }
+        cp_async_commit();
+    }
+    if (tid < W) {
+        const int i = i0 + tid;
+        cs[tid].cm = modes::col(p, i, j);
+        cs[tid].base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
+    }
+    const double alpha_prev = MODE ? cg.alpha[vec] : 0.0;
+    const double beta = MODE ? cg.beta[vec] : 0.0;
+    cp_async_wait0();
+    __syncthreads();
+    const int w = tid % W;
+    const ColS& c = cs[w];
+    const size_t gcol = col0 + w;
+    // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
+#pragma unroll 1
+    for (int e = tid; e < TE; e += NT) {
+        const int k = e / W;
+        double2 u1 = sm[e], u2 = sm[TE + e];
+        if (MODE == 1) {
+            const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
+            const double2 x1 = sm[4 * TE + e], x2 = sm[5 * TE + e];
+            double2* xg = Xcg + (size_t)vec * 2 * n + gcol + kstride * k;
+            xg[0] = make_double2(fma(alpha_prev, q1.x, x1.x), fma(alpha_prev, q1.y, x1.y));   // x += alpha_prev p
+            xg[n] = make_double2(fma(alpha_prev, q2.x, x2.x), fma(alpha_prev, q2.y, x2.y));
+            u1 = make_double2(fma(beta, q1.x, u1.x), fma(beta, q1.y, u1.y));   // p <- r + beta p
+            u2 = make_double2(fma(beta, q2.x, u2.x), fma(beta, q2.y, u2.y));
+            double2* pg = Pcg + (size_t)vec * 2 * n + gcol + kstride * k;
+            pg[0] = u1;
+            pg[n] = u2;
+        }
+        const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
+        Coef o;
+        const long long idx = c.cm.idx0 + (long long)kstride * k;
+        modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
+        const double2 U1 = cscale(u1, o.f1), U2 = cscale(u2, o.f2);
+        sm[e] = modes::comb(o, 0, U1, U2);           // component tiles alias the consumed inputs
+        sm[TE + e] = modes::comb(o, 1, U1, U2);
+        sm[2 * TE + e] = modes::comb(o, 2, U1, U2);
+    }
+    __syncthreads();
+    // ---- phase B: z-DFT of component l over k, twiddle, store ----
+    {
+        const int l = tid / (W * N2), t = (tid / W) % N2;
+        double2* ct = sm + (size_t)l * TE;
+        double2 v[N1];
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
         __syncthreads();
-        // ---- phase B: z-DFT of component l over k, twiddle, store ----
-        {
-            const int l = tid / (W * N2), t = (tid / W) % N2;
-            double2* ct = Ct + (size_t)l * TE;
-            double2 v[N1];
+        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
+        const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+        const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
+        const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
+        const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
+        double2* out = U + (size_t)vec * 3 * n + (size_t)l * n + gcol;
+        double2 au = wt;
 #pragma unroll
-            for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
-            __syncthreads();
-            fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
-            const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
-            const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
-            const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
-            const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
-            double2* out = U + (size_t)ti.vec * 3 * n + (size_t)l * n + gcol;
-            double2 au = wt;
+        for (int u = 0; u < N1 / N2; ++u) {
+            double2 f = au;
 #pragma unroll
-            for (int u = 0; u < N1 / N2; ++u) {
-                double2 f = au;
-#pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) {
-                    const int cc = t + N2 * u + N1 * k2;
-                    out[kstride * cc] = cmul(v[u * N2 + k2], f);
-                    f = cmul(f, wk);
-                }
-                au = cmul(au, wu);
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int cc = t + N2 * u + N1 * k2;
+                out[kstride * cc] = cmul(v[u * N2 + k2], f);
+                f = cmul(f, wk);
             }
+            au = cmul(au, wu);
         }
-        __syncthreads();   // stage (it & 1), Ct and cs are free
     }
 }
 
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 1)
-    k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, int nvec, CGFuse cg) {
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
+    k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
-    constexpr int N = C::N, NT = C::NT, TE = C::TE, S = C::S;
-    constexpr int NA = MODE ? 5 : 3;   // staged arrays: U0 U1 U2 | r1 r2
-    extern __shared__ double2 sm[];
-    double2* stage = sm;                    // [2][NA][TE]
-    double2* hroot = sm + 2 * NA * TE;      // [N]
+    constexpr int NT = C::NT, TE = C::TE;
+    extern __shared__ double2 sm[];   // [NA][TE]: U0 U1 U2 | r1 r2
     __shared__ ColS cs[W];
     __shared__ double2 red[32];
-    __shared__ double acc[8];
     const ModeP& p = a.mp;
     const long long n = p.n;
-    const int n1 = p.n1, n2 = p.n2;
-    const int nit = n1 / W;
-    const int ntiles = nit * n2 * nvec;
-    const size_t kstride = (size_t)n1 * n2;
+    const int n1 = p.n1;
+    const size_t kstride = (size_t)n1 * p.n2;
     const int tid = threadIdx.x;
-    for (int k = tid; k < N; k += NT) hroot[k] = __ldg(a.hroot_z + k);
-    if (MODE == 1 && tid < 8) acc[tid] = 0.0;
-
-    auto issue = [&](int tile, int st) {
-        const TileIdx ti = tile_of(tile, nit, n2);
-        const size_t col0 = (size_t)ti.i0 * W + (size_t)n1 * ti.j;
-        double2* dst = stage + (size_t)st * NA * TE;
-        const double2* u0 = U + (size_t)ti.vec * 3 * n;
-#pragma unroll 1
+    const int i0 = blockIdx.x * W, j = blockIdx.y, vec = blockIdx.z;
+    const size_t col0 = (size_t)i0 + (size_t)n1 * j;
+    {
+        const double2* u0 = U + (size_t)vec * 3 * n + col0;
+        const double2* r1 = MODE ? OUT + (size_t)vec * 2 * n + col0 : nullptr;
+#pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
-            const int k = q / W, w = q - k * W;
-            const size_t g = col0 + w + kstride * k;
-            cp_async16(dst + q, u0 + g);
-            cp_async16(dst + TE + q, u0 + n + g);
-            cp_async16(dst + 2 * TE + q, u0 + 2 * n + g);
+            const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
+            cp_async16(sm + q, u0 + g);
+            cp_async16(sm + TE + q, u0 + n + g);
+            cp_async16(sm + 2 * TE + q, u0 + 2 * n + g);
             if (MODE == 1) {
-                const double2* r1 = OUT + (size_t)ti.vec * 2 * n;
-                cp_async16(dst + 3 * TE + q, r1 + g);
-                cp_async16(dst + 4 * TE + q, r1 + n + g);
+                cp_async16(sm + 3 * TE + q, r1 + g);
+                cp_async16(sm + 4 * TE + q, r1 + n + g);
             }
         }
-    };
-
-    int tile = blockIdx.x;
-    if (tile < ntiles) issue(tile, 0);
-    cp_async_commit();
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-        const int nxt = tile + gridDim.x;
-        if (nxt < ntiles) issue(nxt, (it + 1) & 1);
         cp_async_commit();
-        const TileIdx ti = tile_of(tile, nit, n2);
-        col_setup<W>(p, ti, cs);
-        cp_async_wait1();
-        __syncthreads();
-        double2* sg = stage + (size_t)(it & 1) * NA * TE;
-        const int w = tid % W;
-        const ColS& c = cs[w];
-        const size_t gcol = (size_t)ti.i0 * W + w + (size_t)n1 * ti.j;
-        // ---- phase B: conj twiddle, z-DFT (-) of component l over c ----
-        {
-            const int l = tid / (W * N2), t = (tid / W) % N2;
-            double2* ct = sg + (size_t)l * TE;
-            const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
-            double2 f = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
-            const double2 wu = conj2(tw_at(a.tw, ((unsigned long long)N2 * N3) % nn));
-            double2 v[N1];
+    }
+    if (tid < W) {
+        const int i = i0 + tid;
+        cs[tid].cm = modes::col(p, i, j);
+        cs[tid].base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
+    }
+    const double alpha = MODE == 1 ? cg.alpha[vec] : 0.0;
+    cp_async_wait0();
+    __syncthreads();
+    const int w = tid % W;
+    const ColS& c = cs[w];
+    const size_t gcol = col0 + w;
+    // ---- phase B: conj twiddle, z-DFT (-) of component l over c ----
+    {
+        const int l = tid / (W * N2), t = (tid / W) % N2;
+        double2* ct = sm + (size_t)l * TE;
+        const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+        double2 f = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
+        const double2 wu = conj2(tw_at(a.tw, ((unsigned long long)N2 * N3) % nn));
+        double2 v[N1];
 #pragma unroll
-            for (int m = 0; m < N1; ++m) {
-                v[m] = cmul(ct[(N2 * m + t) * W + w], f);
-                f = cmul(f, wu);
-            }
-            __syncthreads();
-            fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
-#pragma unroll
-            for (int u = 0; u < N1 / N2; ++u)
-#pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) ct[(t + N2 * u + N1 * k2) * W + w] = v[u * N2 + k2];
+        for (int m = 0; m < N1; ++m) {
+            v[m] = cmul(ct[(N2 * m + t) * W + w], f);
+            f = cmul(f, wu);
         }
         __syncthreads();
-        // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
-        double rr = 0.0;
-        const double alpha = MODE == 1 ? cg.alpha[ti.vec] : 0.0;
-        double2* o1 = OUT + (size_t)ti.vec * 2 * n + gcol;
+        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int e = tid + s * NT;
-            if (e < TE) {
-                const int k = e / W;
-                const double2 l2 = modes::lam3(p, c.cm, hroot[k]);
-                Coef o;
-                const long long idx = c.cm.idx0 + (long long)kstride * k;
-                modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
-                const double2 w0 = sg[e], w1 = sg[TE + e], w2 = sg[2 * TE + e];
-                double2 z1 = cadd3(cjm(o.num1[0], w0), cjm(o.num1[1], w1), cjm(o.num1[2], w2));
-                double2 z2 = cadd3(cmul(o.d[0], w0), cmul(o.d[1], w1), cmul(o.d[2], w2));
-                z1 = cscale(z1, o.f1);
-                z2 = cscale(z2, o.f2);
-                if (MODE == 1) {
-                    double2 r1 = sg[3 * TE + e], r2 = sg[4 * TE + e];
-                    r1 = make_double2(fma(-alpha, z1.x, r1.x), fma(-alpha, z1.y, r1.y));
-                    r2 = make_double2(fma(-alpha, z2.x, r2.x), fma(-alpha, z2.y, r2.y));
-                    o1[kstride * k] = r1;
-                    o1[n + kstride * k] = r2;
-                    rr += fma(r1.x, r1.x, fma(r1.y, r1.y, fma(r2.x, r2.x, r2.y * r2.y)));
-                } else {
-                    o1[kstride * k] = z1;
-                    o1[n + kstride * k] = z2;
-                }
-            }
-        }
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) ct[(t + N2 * u + N1 * k2) * W + w] = v[u * N2 + k2];
+    }
+    __syncthreads();
+    // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
+    double rr = 0.0;
+    double2* o1 = OUT + (size_t)vec * 2 * n + gcol;
+#pragma unroll 1
+    for (int e = tid; e < TE; e += NT) {
+        const int k = e / W;
+        const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
+        Coef o;
+        const long long idx = c.cm.idx0 + (long long)kstride * k;
+        modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
+        const double2 w0 = sm[e], w1 = sm[TE + e], w2 = sm[2 * TE + e];
+        double2 z1 = cadd3(cjm(o.num1[0], w0), cjm(o.num1[1], w1), cjm(o.num1[2], w2));
+        double2 z2 = cadd3(cmul(o.d[0], w0), cmul(o.d[1], w1), cmul(o.d[2], w2));
+        z1 = cscale(z1, o.f1);
+        z2 = cscale(z2, o.f2);
         if (MODE == 1) {
-            const double2 bs = block_sum(make_double2(rr, 0.0), red);
-            if (tid == 0) acc[ti.vec] += bs.x;
+            double2 r1 = sm[3 * TE + e], r2 = sm[4 * TE + e];
+            r1 = make_double2(fma(-alpha, z1.x, r1.x), fma(-alpha, z1.y, r1.y));
+            r2 = make_double2(fma(-alpha, z2.x, r2.x), fma(-alpha, z2.y, r2.y));
+            o1[kstride * k] = r1;
+            o1[n + kstride * k] = r2;
+            rr += fma(r1.x, r1.x, fma(r1.y, r1.y, fma(r2.x, r2.x, r2.y * r2.y)));
+        } else {
+            o1[kstride * k] = z1;
+            o1[n + kstride * k] = z2;
         }
-        __syncthreads();   // stage (it & 1) and cs are free
     }
     if (MODE == 1) {
-        // per-CTA partials of (r, r) for every vector; the last CTA forms beta
-        const int nb = gridDim.x;
-        if (tid < nvec) cg.part_z[(size_t)tid * nb + blockIdx.x] = acc[tid];
-        __syncthreads();
-        if (cg_last_block(cg.counter + 1, gridDim.x, red)) cg_finish_beta(cg, nb, nvec, red);
+        // per-CTA partial of (r, r); the last CTA of the launch forms beta
+        const int nb = gridDim.x * gridDim.y;
+        cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, red);
+        if (cg_last_block(cg.counter + 1, nb * gridDim.z, red)) cg_finish_beta(cg, nb, gridDim.z, red);
     }
 }
 
@@ -374,21 +292,8 @@ __global__ void k_cg_xfinal(double2* __restrict__ X, const double2* __restrict__
 template <int N1, int N2, int W>
 struct ZLaunch {
     using C = ZCfg<N1, N2, W>;
-    static size_t smem_fwd(int mode) { return (size_t)(2 * (mode ? 4 : 2) * C::TE + 3 * C::TE + C::N) * sizeof(double2); }
-    static size_t smem_adj(int mode) { return (size_t)(2 * (mode ? 5 : 3) * C::TE + C::N) * sizeof(double2); }
-    template <class K>
-    static int grid(K kern, size_t smem, int ntiles) {
-        static int per_sm = -1;
-        static int nsm = 0;
-        if (per_sm < 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, smem);
-            if (per_sm < 1) per_sm = 1;
-        }
-        return std::max(1, std::min(ntiles, nsm * per_sm));
-    }
+    static size_t smem_fwd(int mode) { return (size_t)(mode ? 6 : 3) * C::TE * sizeof(double2); }
+    static size_t smem_adj(int mode) { return (size_t)(mode ? 5 : 3) * C::TE * sizeof(double2); }
 };
 
 }  // namespace
@@ -411,17 +316,17 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_fwd(mode);
-    const int ntiles = (a.mp.n1 / W) * a.mp.n2 * nvec;
+    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
     if (mode) {
         auto kern = k_zfwd2<N1, N2, W, 1>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(Y, U, a, 1, nvec, P, X, *cg);
+        kern<<<g, L::C::NT, smem, st>>>(Y, U, a, 1, P, X, *cg);
     } else {
         auto kern = k_zfwd2<N1, N2, W, 0>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(Y, U, a, op, nvec, nullptr, nullptr, CGFuse{});
+        kern<<<g, L::C::NT, smem, st>>>(Y, U, a, op, nullptr, nullptr, CGFuse{});
     }
     return cudaGetLastError();
 }
@@ -432,17 +337,17 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_adj(mode);
-    const int ntiles = (a.mp.n1 / W) * a.mp.n2 * nvec;
+    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
     if (mode) {
         auto kern = k_zadj2<N1, N2, W, 1>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(U, OUT, a, 1, nvec, *cg);
+        kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, 1, *cg);
     } else {
         auto kern = k_zadj2<N1, N2, W, 0>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<L::grid(kern, smem, ntiles), L::C::NT, smem, st>>>(U, OUT, a, op, nvec, CGFuse{});
+        kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, op, CGFuse{});
     }
     return cudaGetLastError();
 }
