@@ -53,6 +53,7 @@ struct OpArgs {
     int comp0;               // first component slab (vector*3 + l) of a split y/x launch
     int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
+    int plane_cw;            // plane pass: columns per CTA (32 default, 16 = twice the cluster size)
 };
 
 struct Profiler;  // host-side, see solver.cu

@@ -267,6 +267,15 @@ bool plane_supported(const OpArgs& a) {
 }
 
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    if (a.plane_cw == 16) {   // 16 columns per CTA: smaller CTAs, twice the cluster size
+        switch (a.mp.n1) {
+            case 64: return launch_plane_t<8, 8, 4>(a, U, nslab, cg, st);
+            case 96: return launch_plane_t<24, 4, 6>(a, U, nslab, cg, st);
+            case 128: return launch_plane_t<16, 8, 8>(a, U, nslab, cg, st);
+            case 256: return launch_plane_t<16, 16, 16>(a, U, nslab, cg, st);
+            default: break;
+        }
+    }
     switch (a.mp.n1) {
 #define BNF_CASE(NN, A, B, PP) case NN: return launch_plane_t<A, B, PP>(a, U, nslab, cg, st);
         BNF_PLANE_PLANS(BNF_CASE)

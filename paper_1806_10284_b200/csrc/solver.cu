@@ -853,6 +853,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
+    if (const char* cw = std::getenv("BNF_PLANE_CW")) s->args.plane_cw = std::atoi(cw);
     CK(s->iterbuf.ensure(4 * sizeof(int)));
     CK(cudaMemset(s->iterbuf.p, 0, 4 * sizeof(int)));
     s->d_iter = s->iterbuf.as<int>();

@@ -261,3 +261,19 @@ def test_full_size_eigenvalues_vs_oracle(bnf, golden_dir, fname):
     assert h == g["eps_sha256_16"]
     lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
     np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+
+
+def test_graph_cg_equals_eager(bnf):
+    """The CG loop as one CUDA graph (device-side while condition) and the
+    eager, per-kernel-timed loop (bnf_set_profile) run the same kernels:
+    identical eigenvalues and matvec counts, bit for bit."""
+    cfg, n, kap = _cfg_case(2, (16, 16, 16), 9)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    S.set_profile(0)
+    l1, s1 = S.solve(kap, 8)
+    S.set_profile(1)
+    l2, s2 = S.solve(kap, 8)
+    S.set_profile(0)
+    assert np.array_equal(l1, l2)
+    assert s1["matvecs"] == s2["matvecs"] and s1["inner_iters"] == s2["inner_iters"]
+    assert s1["kernel_launches"] > 0 and s2["kernel_launches"] > 0
