@@ -176,6 +176,12 @@ int bnf_kernel_times_reset(bnf_solver* s);
    per iteration).  Both paths execute the same kernels on the same data. */
 int bnf_set_profile(bnf_solver* s, int on);
 
+/* Diagnostics: per-phase clock64() cycle sums of the plane pass, collected
+   only when the solver was created with the environment variable
+   BNF_PHASE_PROF set (thread 0 of every CTA; entry 15 = CTA count).  Copies
+   min(cap, 16) counters to out (HOST) and resets them. */
+int bnf_phase_counters(bnf_solver* s, unsigned long long* out, int cap);
+
 const char* bnf_last_error(void);
 int bnf_version(void);
 

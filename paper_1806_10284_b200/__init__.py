@@ -73,6 +73,7 @@ _sigs = {
                          C.POINTER(C.c_int)],
     "bnf_kernel_times_reset": [_P],
     "bnf_set_profile": [_P, C.c_int],
+    "bnf_phase_counters": [_P, _P, C.c_int],
     "bnf_host_herm_eig": [C.c_int, _P, _P, _P],
 }
 for _name, _args in _sigs.items():
@@ -87,7 +88,7 @@ _lib.bnf_opts_default.restype = None
 
 EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce",
            "bnf_opts_default", "bnf_solver_create", "bnf_solver_destroy", "bnf_set_epsilon", "bnf_set_kappa",
-           "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile",
+           "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile", "bnf_phase_counters",
            "bnf_last_error", "bnf_version", "bnf_host_herm_eig"]
 
 
@@ -210,6 +211,12 @@ class Solver:
     def set_profile(self, on):
         """Per-kernel CUDA-event timing on/off (off: CG loop as one CUDA graph)."""
         _check(_lib.bnf_set_profile(self._h, int(bool(on))))
+
+    def phase_counters(self):
+        """Plane-pass per-phase cycle sums (BNF_PHASE_PROF set at creation); resets them."""
+        out = np.zeros(16, dtype=np.uint64)
+        _check(_lib.bnf_phase_counters(self._h, out.ctypes.data_as(C.c_void_p), 16))
+        return out
 
     def close(self):
         if getattr(self, "_h", None):

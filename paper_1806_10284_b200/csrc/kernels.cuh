@@ -54,6 +54,7 @@ struct OpArgs {
     int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
     int plane_cw;            // plane pass: columns per CTA (32 default, 16 = twice the cluster size)
+    unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
 };
 
 struct Profiler;  // host-side, see solver.cu

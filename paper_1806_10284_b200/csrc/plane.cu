@@ -86,12 +86,24 @@ struct PlaneCfg {
     static constexpr int SMEM = CW * N1 * (N2 + 1);
 };
 
+// Optional per-phase cycle accounting (OpArgs::prof != null, bnf_phase_counters):
+// thread 0 of every CTA adds the clock64() delta of each phase to prof[k].
+#define BNF_PROBE(k)                                                     \
+    do {                                                                 \
+        if (a.prof != nullptr && threadIdx.x == 0) {                     \
+            const long long now_ = clock64();                            \
+            atomicAdd(a.prof + (k), (unsigned long long)(now_ - t_last)); \
+            t_last = now_;                                               \
+        }                                                                \
+    } while (0)
+
 template <int N1, int N2, int P, int CG>
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
     extern __shared__ double2 D[];
     const ModeP& p = a.mp;
+    long long t_last = clock64();
     const unsigned r = Cluster<P>::rank();
     const int c = blockIdx.x / P;
     const int vl = blockIdx.y + a.comp0;
@@ -119,6 +131,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
     for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
     fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+    BNF_PROBE(0);   // load + y-FFT
     {
         // e^{-2 pi i b M / n12} for b = t + N2 u + N1 k2: w^t (w^N2)^u (w^N1)^k2
         const unsigned Pt = ((unsigned)t * M) % n12;
@@ -141,7 +154,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     }
     // exchange Y -> X: element (b, i) goes to CTA b / CW, row b % CW, column i
     const unsigned dbase = (unsigned)__cvta_generic_to_shared(D);
+    BNF_PROBE(1);   // twiddle
     Cluster<P>::sync_relaxed();   // every CTA is done with its own D
+    BNF_PROBE(2);   // barrier 1
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -149,8 +164,10 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             const int b = t + N2 * u + N1 * k2;
             Cluster<P>::put(D, dbase, (unsigned)(b / CW), (b % CW) * N + i, v[u * N2 + k2]);
         }
+    BNF_PROBE(3);   // DSMEM stores Y->X
     if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     Cluster<P>::sync();
+    BNF_PROBE(4);   // barrier 2
 
     // ---------------- phase X: rows b = r*CW + rw, FFT over i ----------------
     const int tx = tid % N2, rw = tid / N2;
@@ -159,6 +176,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     for (int m = 0; m < N1; ++m) v[m] = D[rw * N + N2 * m + tx];
     __syncthreads();   // D becomes the transpose buffer
     fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    BNF_PROBE(5);   // x-FFT
     double pmp = 0.0;
     {
         const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
@@ -186,15 +204,20 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D)) cg_finish_alpha(cgf, nb, nvec_all, D);
         __syncthreads();
     }
+    BNF_PROBE(6);   // eps (+ CG partial)
     fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    BNF_PROBE(7);   // x-FFT*
     // exchange X -> Y: element (b, a) goes to CTA a / CW, row b, column a % CW (ld CW)
     Cluster<P>::sync_relaxed();
+    BNF_PROBE(8);   // barrier 3
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
         const int aa = N2 * m + tx;
         Cluster<P>::put(D, dbase, (unsigned)(aa / CW), b * CW + (aa % CW), v[m]);
     }
+    BNF_PROBE(9);   // DSMEM stores X->Y
     Cluster<P>::sync();
+    BNF_PROBE(10);  // barrier 4
 
     // ---------------- phase Y*: conj twiddle, FFT (-) over b ----------------
     {
@@ -211,6 +234,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     }
     __syncthreads();
     fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+    BNF_PROBE(11);  // twiddle* + y-FFT*
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -218,6 +242,8 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             const int j = t + N2 * u + N1 * k2;
             plane[(size_t)j * N + i] = v[u * N2 + k2];
         }
+    BNF_PROBE(12);  // stores issued
+    if (a.prof != nullptr && threadIdx.x == 0) atomicAdd(a.prof + 15, 1ull);   // CTA count
 }
 
 template <int N1, int N2, int P>
@@ -267,6 +293,7 @@ bool plane_supported(const OpArgs& a) {
 }
 
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    if (a.plane_cw == 64 && a.mp.n1 == 128) return launch_plane_t<16, 8, 2>(a, U, nslab, cg, st);
     if (a.plane_cw == 16) {   // 16 columns per CTA: smaller CTAs, twice the cluster size
         switch (a.mp.n1) {
             case 64: return launch_plane_t<8, 8, 4>(a, U, nslab, cg, st);

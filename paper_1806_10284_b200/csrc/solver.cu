@@ -199,6 +199,7 @@ struct bnf_solver {
     int cgg_next = 0;
     cudaStream_t cap = nullptr;   // capture stream
     long long kver = 0;           // bumped whenever OpArgs change (kappa, eps)
+    DevBuf phasebuf;              // per-phase cycle counters (BNF_PHASE_PROF)
     DevBuf iterbuf;               // int[3]: per-call CG iterations, total iterations, total vector-iterations
     int* d_iter = nullptr;
     int graph_kernels_per_iter = 0;
@@ -854,6 +855,9 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
     if (const char* cw = std::getenv("BNF_PLANE_CW")) s->args.plane_cw = std::atoi(cw);
+    CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
+    CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
+    s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;
     CK(s->iterbuf.ensure(4 * sizeof(int)));
     CK(cudaMemset(s->iterbuf.p, 0, 4 * sizeof(int)));
     s->d_iter = s->iterbuf.as<int>();
@@ -1249,6 +1253,17 @@ int bnf_kernel_times(bnf_solver* s, const char** names, double* ms, long long* l
         ++k;
     }
     *count = k;
+    return BNF_OK;
+}
+
+int bnf_phase_counters(bnf_solver* s, unsigned long long* out, int cap) {
+    if (!s || !out || cap < 1) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpy(out, s->phasebuf.p, sizeof(unsigned long long) * std::min(cap, 16), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     return BNF_OK;
 }
 

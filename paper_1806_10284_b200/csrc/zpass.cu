@@ -28,6 +28,10 @@
 #include "kernels.cuh"
 #include "modes.cuh"
 
+#ifndef BNF_Z_MINB
+#define BNF_Z_MINB 3   // resident CTAs per SM the z passes are compiled for
+#endif
+
 namespace bnf {
 namespace {
 
@@ -74,12 +78,12 @@ struct ColS {   // per-column constants shared through smem
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
-    extern __shared__ double2 sm[];   // [NA][TE]: y1 y2 (+1) | r1 r2 p1 p2 x1 x2; Ct = [0..3)
+    extern __shared__ double2 sm[];   // [NA][TE]: y1 y2 (+1) | r1 r2 p1 p2; Ct = [0..3)
     __shared__ ColS cs[W];
     const ModeP& p = a.mp;
     const long long n = p.n;
@@ -91,7 +95,6 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
     {
         const double2* y1 = Y + (size_t)vec * 2 * n + col0;
         const double2* p1 = MODE ? Pcg + (size_t)vec * 2 * n + col0 : nullptr;
-        const double2* x1 = MODE ? Xcg + (size_t)vec * 2 * n + col0 : nullptr;
 #pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
             const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
@@ -100,8 +103,6 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
             if (MODE == 1) {
                 cp_async16(sm + 2 * TE + q, p1 + g);
                 cp_async16(sm + 3 * TE + q, p1 + n + g);
-                cp_async16(sm + 4 * TE + q, x1 + g);
-                cp_async16(sm + 5 * TE + q, x1 + n + g);
             }
         }
         cp_async_commit();
@@ -118,6 +119,13 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
     const int w = tid % W;
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
+    // x is streamed straight from HBM (not staged), one element ahead
+    double2* xcol = MODE ? Xcg + (size_t)vec * 2 * n + gcol : nullptr;
+    double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0);
+    if (MODE == 1 && tid < TE) {
+        xn1 = xcol[kstride * (tid / W)];
+        xn2 = xcol[n + kstride * (tid / W)];
+    }
     // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
 #pragma unroll 1
     for (int e = tid; e < TE; e += NT) {
@@ -125,8 +133,12 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
         double2 u1 = sm[e], u2 = sm[TE + e];
         if (MODE == 1) {
             const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
-            const double2 x1 = sm[4 * TE + e], x2 = sm[5 * TE + e];
-            double2* xg = Xcg + (size_t)vec * 2 * n + gcol + kstride * k;
+            const double2 x1 = xn1, x2 = xn2;
+            if (e + NT < TE) {
+                xn1 = xcol[kstride * ((e + NT) / W)];
+                xn2 = xcol[n + kstride * ((e + NT) / W)];
+            }
+            double2* xg = xcol + kstride * k;
             xg[0] = make_double2(fma(alpha_prev, q1.x, x1.x), fma(alpha_prev, q1.y, x1.y));   // x += alpha_prev p
             xg[n] = make_double2(fma(alpha_prev, q2.x, x2.x), fma(alpha_prev, q2.y, x2.y));
             u1 = make_double2(fma(beta, q1.x, u1.x), fma(beta, q1.y, u1.y));   // p <- r + beta p
@@ -177,11 +189,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
-    extern __shared__ double2 sm[];   // [NA][TE]: U0 U1 U2 | r1 r2
+    extern __shared__ double2 sm[];   // [3][TE]: U0 U1 U2 (r is streamed, not staged)
     __shared__ ColS cs[W];
     __shared__ double2 red[32];
     const ModeP& p = a.mp;
@@ -193,17 +205,12 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
     const size_t col0 = (size_t)i0 + (size_t)n1 * j;
     {
         const double2* u0 = U + (size_t)vec * 3 * n + col0;
-        const double2* r1 = MODE ? OUT + (size_t)vec * 2 * n + col0 : nullptr;
 #pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
             const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
             cp_async16(sm + q, u0 + g);
             cp_async16(sm + TE + q, u0 + n + g);
             cp_async16(sm + 2 * TE + q, u0 + 2 * n + g);
-            if (MODE == 1) {
-                cp_async16(sm + 3 * TE + q, r1 + g);
-                cp_async16(sm + 4 * TE + q, r1 + n + g);
-            }
         }
         cp_async_commit();
     }
@@ -218,6 +225,12 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
     const int w = tid % W;
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
+    double2* o1 = OUT + (size_t)vec * 2 * n + gcol;
+    double2 rn1 = make_double2(0, 0), rn2 = make_double2(0, 0);
+    if (MODE == 1 && tid < TE) {   // first residual element, in flight during the FFT phase
+        rn1 = o1[kstride * (tid / W)];
+        rn2 = o1[n + kstride * (tid / W)];
+    }
     // ---- phase B: conj twiddle, z-DFT (-) of component l over c ----
     {
         const int l = tid / (W * N2), t = (tid / W) % N2;
@@ -241,7 +254,6 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
     __syncthreads();
     // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
     double rr = 0.0;
-    double2* o1 = OUT + (size_t)vec * 2 * n + gcol;
 #pragma unroll 1
     for (int e = tid; e < TE; e += NT) {
         const int k = e / W;
@@ -255,7 +267,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, 2)
         z1 = cscale(z1, o.f1);
         z2 = cscale(z2, o.f2);
         if (MODE == 1) {
-            double2 r1 = sm[3 * TE + e], r2 = sm[4 * TE + e];
+            double2 r1 = rn1, r2 = rn2;
+            if (e + NT < TE) {
+                rn1 = o1[kstride * ((e + NT) / W)];
+                rn2 = o1[n + kstride * ((e + NT) / W)];
+            }
             r1 = make_double2(fma(-alpha, z1.x, r1.x), fma(-alpha, z1.y, r1.y));
             r2 = make_double2(fma(-alpha, z2.x, r2.x), fma(-alpha, z2.y, r2.y));
             o1[kstride * k] = r1;
@@ -292,8 +308,8 @@ __global__ void k_cg_xfinal(double2* __restrict__ X, const double2* __restrict__
 template <int N1, int N2, int W>
 struct ZLaunch {
     using C = ZCfg<N1, N2, W>;
-    static size_t smem_fwd(int mode) { return (size_t)(mode ? 6 : 3) * C::TE * sizeof(double2); }
-    static size_t smem_adj(int mode) { return (size_t)(mode ? 5 : 3) * C::TE * sizeof(double2); }
+    static size_t smem_fwd(int mode) { return (size_t)(mode ? 4 : 3) * C::TE * sizeof(double2); }
+    static size_t smem_adj(int) { return (size_t)3 * C::TE * sizeof(double2); }
 };
 
 }  // namespace
