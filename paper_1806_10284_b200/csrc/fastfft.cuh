@@ -237,6 +237,9 @@ __device__ __forceinline__ double2 root_tw(const double2* __restrict__ root, int
     return S > 0 ? w : cconj(w);
 }
 
+// `root` is the axis' stage-twiddle table laid out [k1][t]: root[k1 * N2 + t]
+// = e^{2 pi i t k1 / N} (AxisPlan::root2), so the N2 threads of a sequence that
+// sit in one warp read consecutive entries (one wavefront per load).
 // Natural layout -> stage-2 layout.  On exit v[u*N2 + k2] = X[k1 + N1*k2]
 // with k1 = t + N2*u.  Two __syncthreads (buffer free on exit).
 template <int N1, int N2, int S, class X>
@@ -244,7 +247,7 @@ __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2*
     DFT<N1, S>::run(v);
     if (t > 0) {
 #pragma unroll
-        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, t * k1));
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, k1 * N2 + t));
     }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) xch[X::idx(k1, t, w)] = v[k1];
@@ -283,9 +286,73 @@ __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, doubl
     __syncthreads();
     if (t > 0) {
 #pragma unroll
-        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, t * k1));
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, k1 * N2 + t));
     }
     DFT<N1, S>::run(v);
+}
+
+// ------------------------------------------- twiddle sequences (no long chains)
+// w^b for the N1 elements a thread holds after fft_fwd (stage-2 layout,
+// b = t + N2 u + N1 k2) or before it (natural layout, b = N2 m + t), built from
+// the three bases w^t, w^N2, w^N1 with product trees of depth <= 3 instead of
+// one sequential multiplication chain per element (the chain's FP64 latency
+// was exposed).  Multiplies v in place.
+template <int K>
+struct Pow4 {   // g^k = q[k / 4] p[k % 4], k < K
+    static constexpr int R = K < 4 ? K : 4;
+    static constexpr int Q = (K + R - 1) / R;
+    double2 p[R], q[Q];
+    __device__ __forceinline__ explicit Pow4(double2 g) {
+        p[0] = make_double2(1.0, 0.0);
+        if constexpr (R > 1) p[1] = g;
+        if constexpr (R > 2) p[2] = cmul(g, g);
+        if constexpr (R > 3) p[3] = cmul(p[2], g);
+        q[0] = make_double2(1.0, 0.0);
+        if constexpr (Q > 1) {
+            const double2 gR = (R == 4) ? cmul(p[2], p[2]) : (R == 3 ? cmul(p[2], g) : (R == 2 ? p[2 % R] : g));
+            q[1] = gR;
+#pragma unroll
+            for (int s = 2; s < Q; ++s) q[s] = cmul(q[s - 1], gR);
+        }
+    }
+};
+
+template <int N1, int N2>
+__device__ __forceinline__ void twiddle_stage2(double2 (&v)[N1], double2 wt, double2 wN2, double2 wN1) {
+    static_assert(N2 >= 4 || N2 == 2, "twiddle_stage2: N2 in {2} or >= 4");
+    if constexpr (N2 == 2) {
+        double2 au = wt;
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u) {
+            v[u * N2] = cmul(v[u * N2], au);
+            v[u * N2 + 1] = cmul(v[u * N2 + 1], cmul(au, wN1));
+            au = cmul(au, wN2);
+        }
+    } else {
+        const Pow4<N2> B(wN1);
+        double2 au = wt;
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u) {
+            double2 c[Pow4<N2>::Q];
+#pragma unroll
+            for (int s = 0; s < Pow4<N2>::Q; ++s) c[s] = s == 0 ? au : cmul(au, B.q[s]);
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2)
+                v[u * N2 + k2] = cmul(v[u * N2 + k2], (k2 % 4 == 0) ? c[k2 / 4] : cmul(c[k2 / 4], B.p[k2 % 4]));
+            au = cmul(au, wN2);
+        }
+    }
+}
+
+template <int N1, int N2>
+__device__ __forceinline__ void twiddle_natural(double2 (&v)[N1], double2 wt, double2 wN2) {
+    const Pow4<N1> B(wN2);
+    double2 c[Pow4<N1>::Q];
+#pragma unroll
+    for (int s = 0; s < Pow4<N1>::Q; ++s) c[s] = s == 0 ? wt : cmul(wt, B.q[s]);
+#pragma unroll
+    for (int m = 0; m < N1; ++m)
+        v[m] = cmul(v[m], (m % Pow4<N1>::R == 0) ? c[m / Pow4<N1>::R] : cmul(c[m / Pow4<N1>::R], B.p[m % Pow4<N1>::R]));
 }
 
 }  // namespace fast

@@ -762,42 +762,26 @@ __global__ void __launch_bounds__(W * N2) k_ypass_fast(double2* __restrict__ U, 
     const int i = blockIdx.x * W + w, c = blockIdx.y;
     const bool ok = i < p.n1;
     double2* col = U + (size_t)(blockIdx.z + a.comp0) * p.n + (size_t)p.n1 * (size_t)p.n2 * c + (ok ? i : 0);
-    // twiddle e^{-+2 pi i b M / n12}, M = m1 i; phase index P(b) = b M mod n12 kept incrementally
-    const unsigned long long n12 = (unsigned long long)p.n12;
-    const unsigned long long M = mulmod((unsigned long long)p.m1, (unsigned long long)(ok ? i : 0), n12);
-    const unsigned long long Pt = mulmod((unsigned long long)t, M, n12);
+    // twiddle e^{-+2 pi i b M / n12}, M = m1 i: products of w^t, w^N2, w^N1 (fastfft twiddle_*)
+    const unsigned n12 = (unsigned)p.n12;
+    const unsigned M = ((unsigned)p.m1 * (unsigned)(ok ? i : 0)) % n12;
     const unsigned long long s3 = (unsigned long long)p.n3;
+    const double2 wt = tw_lookup(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
+    const double2 wu = tw_lookup(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
     double2 v[N1];
-    {
-        const unsigned long long D = mulmod((unsigned long long)N2, M, n12);
-        unsigned long long P = Pt;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) {
-            const int j = N2 * m + t;
-            double2 x = ok ? col[(size_t)p.n1 * j] : make_double2(0, 0);
-            if (ADJ) x = cmul(x, tw_lookup(a.tw, P * s3));          // conj of e^{-2pi i b M/n12}
-            v[m] = x;
-            P = mod_add(P, D, n12);
-        }
-    }
-    fast::fft_fwd<N1, N2, ADJ ? -1 : 1, X>(v, t, w, sm, a.py.root);
+    for (int m = 0; m < N1; ++m) v[m] = ok ? col[(size_t)p.n1 * (N2 * m + t)] : make_double2(0, 0);
+    if (ADJ) fast::twiddle_natural<N1, N2>(v, wt, wu);   // e^{+2 pi i b M / n12}, b = N2 m + t
+    fast::fft_fwd<N1, N2, ADJ ? -1 : 1, X>(v, t, w, sm, a.py.root2);
     if (ok) {
-        const unsigned long long Du = mulmod((unsigned long long)N2, M, n12);
-        const unsigned long long Dk = mulmod((unsigned long long)N1, M, n12);
-        unsigned long long Pu = Pt;
-#pragma unroll
-        for (int u = 0; u < N1 / N2; ++u) {
-            unsigned long long P = Pu;
-#pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                const int b = t + N2 * u + N1 * k2;
-                double2 x = v[u * N2 + k2];
-                if (!ADJ) x = cmul(x, tw_lookup(a.tw, (P == 0 ? 0ull : n12 - P) * s3));
-                col[(size_t)p.n1 * b] = x;
-                P = mod_add(P, Dk, n12);
-            }
-            Pu = mod_add(Pu, Du, n12);
+        if (!ADJ) {
+            const double2 wk = tw_lookup(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3);
+            fast::twiddle_stage2<N1, N2>(v, cconj(wt), cconj(wu), cconj(wk));   // e^{-2 pi i b M / n12}
         }
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) col[(size_t)p.n1 * (t + N2 * u + N1 * k2)] = v[u * N2 + k2];
     }
 }
 
@@ -818,7 +802,7 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
     double2 v[N1];
 #pragma unroll
     for (int m = 0; m < N1; ++m) v[m] = ok ? row[N2 * m + t] : make_double2(0, 0);
-    fast::fft_fwd<N1, N2, 1, X>(v, t, w, sm, a.px.root);
+    fast::fft_fwd<N1, N2, 1, X>(v, t, w, sm, a.px.root2);
     double pmp = 0.0;
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
@@ -838,7 +822,7 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm)) cg_finish_alpha(cg, nb, nvec_all, sm);
     }
-    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root);
+    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
     if (ok) {
 #pragma unroll
         for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
@@ -920,7 +904,7 @@ __global__ void __launch_bounds__(3 * W * N2) k_zfwd_fast(const double2* __restr
 #pragma unroll
     for (int m = 0; m < N1; ++m) v[m] = tile[(N2 * m + t) * W + w];
     __syncthreads();
-    fast::fft_fwd<N1, N2, 1, X>(v, t, w, tile, a.pz.root);
+    fast::fft_fwd<N1, N2, 1, X>(v, t, w, tile, a.pz.root2);
     if (ok) {
         const unsigned long long nn = (unsigned long long)n;
         const unsigned long long N3 = yz_base(p, i, j);
@@ -973,7 +957,7 @@ __global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restr
             P = mod_add(P, D, nn);
         }
     }
-    fast::fft_fwd<N1, N2, -1, X>(v, t, w, tile, a.pz.root);
+    fast::fft_fwd<N1, N2, -1, X>(v, t, w, tile, a.pz.root2);
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -1290,6 +1274,15 @@ cudaError_t launch_cg_p(double2* P, const double2* R, const CGState& s, long lon
     return cudaGetLastError();
 }
 
+
+int fast_split_N2(int N) {
+    switch (N) {
+#define BNF_CASE(NN, A, B) case NN: return B;
+        BNF_FAST_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return 0;
+    }
+}
 
 bool fast_all(const OpArgs& a) { return a.fast && has_fast(a.mp.n1) && has_fast(a.mp.n2) && has_fast(a.mp.n3); }
 

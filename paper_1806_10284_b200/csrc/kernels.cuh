@@ -12,7 +12,8 @@ struct AxisPlan {
     int N;
     int nst;
     int R[12];
-    const double2* root;
+    const double2* root;    // e^{2 pi i t / N}, t < N (generic Stockham passes)
+    const double2* root2;   // fast plan N = N1*N2: e^{2 pi i t k1 / N} at [k1 * N2 + t] (fastfft.cuh)
 };
 
 // Per-k mode parameters.  Fourier mode (i,j,k):
@@ -55,6 +56,8 @@ struct OpArgs {
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
     int plane_cw;            // plane pass: columns per CTA (32 default, 16 = twice the cluster size)
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
+    int plane_persist;          // plane pass: persistent clusters (1) or one cluster per plane (0)
+    long long plane_stagger;    // plane pass: start delay (cycles) of the second half of the clusters
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -94,6 +97,8 @@ cudaError_t launch_bloch_phase(const OpArgs& a, double2* U, int nvec, double kap
                                cudaStream_t st);
 
 bool fast_all(const OpArgs& a);
+// N2 of the register-FFT plan N = N1 * N2 for axis length N, 0 if none
+int fast_split_N2(int N);
 cudaError_t launch_zfwd_cg(const OpArgs& a, const double2* R, double2* P, double2* U, int nvec, const CGFuse& cg,
                            cudaStream_t st);
 cudaError_t launch_xpass_cg(const OpArgs& a, double2* U, int nvec, const CGFuse& cg, cudaStream_t st);

@@ -21,6 +21,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "cgfuse.cuh"
 #include "fastfft.cuh"
 #include "kernels.cuh"
@@ -98,29 +100,62 @@ struct PlaneCfg {
     } while (0)
 
 template <int N1, int N2, int P, int CG>
-__global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
+__global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane(double2* __restrict__ U, OpArgs a, CGFuse cgf, int nslab) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
     extern __shared__ double2 D[];
+    __shared__ double acc_s[8];   // CG: this CTA's (p, M p) partial per vector
     const ModeP& p = a.mp;
     long long t_last = clock64();
     const unsigned r = Cluster<P>::rank();
-    const int c = blockIdx.x / P;
-    const int vl = blockIdx.y + a.comp0;
-    const int l = vl % 3;
     const int tid = threadIdx.x;
+    constexpr bool EPF = (N % 16) == 0;
+    unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);
+    double* lut_s = reinterpret_cast<double*>(eps_s + CW * N);   // the <= 256-entry 1/eps table
+    const bool epf = EPF && a.eps_idx != nullptr;
+    if (epf)
+        for (int q = threadIdx.x; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
+    if (CG && tid < 8) acc_s[tid] = 0.0;
+    // Persistent clusters loop over the planes (component slab, z-plane).  The
+    // second half of the clusters starts half a plane late so that the two
+    // CTAs sharing an SM stay out of phase (one in its FFT phases while the
+    // other streams or exchanges).
+    const int ncl = gridDim.x / P, cid = blockIdx.x / P;
+    const int total = p.n3 * nslab;
+    if (a.plane_stagger > 0 && cid >= ncl / 2) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < a.plane_stagger) {
+        }
+        t_last = clock64();
+    }
+    for (int pl = cid; pl < total; pl += ncl) {
+    const int c = pl % p.n3;
+    const int vl = pl / p.n3 + a.comp0;
+    const int l = vl % 3;
     double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
     double2 v[N1];
     // B^{-1} material indices of this CTA's phase-X rows (contiguous CW*N bytes), prefetched
-    constexpr bool EPF = (N % 16) == 0;
-    unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);
-    const bool epf = EPF && a.eps_idx != nullptr;
     if (epf) {
         const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * ((size_t)r * CW + (size_t)N * c);
         for (int q = threadIdx.x; q < CW * N / 16; q += C::NT) cp_async16(eps_s + 16 * q, src + 16 * q);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
 
+    // L2 prefetch of this CTA's share of the next plane (rows of CW elements,
+    // and its eps rows) so that the next iteration's loads hit L2, not DRAM
+    if (a.plane_persist && tid < 32 && pl + ncl < total) {
+        const int c2 = (pl + ncl) % p.n3, vl2 = (pl + ncl) / p.n3 + a.comp0;
+        const double2* nxt = U + (size_t)vl2 * p.n + (size_t)c2 * N * N + (size_t)r * CW;
+        for (int j = tid; j < N; j += 32) {
+            const unsigned long long ga = (unsigned long long)(nxt + (size_t)j * N);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(ga), "r"((unsigned)(CW * 16)) : "memory");
+        }
+        if (epf && tid == 0) {
+            const unsigned char* e2 = a.eps_idx + (size_t)(vl2 % 3) * p.n + (size_t)N * ((size_t)r * CW + (size_t)N * c2);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((unsigned long long)e2),
+                         "r"((unsigned)(CW * N)) : "memory");
+        }
+    }
     // ---------------- phase Y: columns i = r*CW + w, FFT over j ----------------
     const int w = tid % CW, t = tid / CW;
     const int i = (int)r * CW + w;
@@ -130,7 +165,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;   // m1 i mod n12
 #pragma unroll
     for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
-    fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+    fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
     BNF_PROBE(0);   // load + y-FFT
     {
         // e^{-2 pi i b M / n12} for b = t + N2 u + N1 k2: w^t (w^N2)^u (w^N1)^k2
@@ -140,17 +175,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const double2 wt = conj2(tw_at(a.tw, Pt * s3));
         const double2 wu = conj2(tw_at(a.tw, Pu * s3));
         const double2 wk = conj2(tw_at(a.tw, Pk * s3));
-        double2 au = wt;
-#pragma unroll
-        for (int u = 0; u < N1 / N2; ++u) {
-            double2 f = au;
-#pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                v[u * N2 + k2] = cmul(v[u * N2 + k2], f);
-                f = cmul(f, wk);
-            }
-            au = cmul(au, wu);
-        }
+        fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
     }
     // exchange Y -> X: element (b, i) goes to CTA b / CW, row b % CW, column i
     const unsigned dbase = (unsigned)__cvta_generic_to_shared(D);
@@ -175,7 +200,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
     for (int m = 0; m < N1; ++m) v[m] = D[rw * N + N2 * m + tx];
     __syncthreads();   // D becomes the transpose buffer
-    fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
     BNF_PROBE(5);   // x-FFT
     double pmp = 0.0;
     {
@@ -185,7 +210,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
                 const int aa = tx + N2 * u + N1 * k2;
-                const double e_ = epf ? __ldg(a.eps_lut + eps_s[rw * N + aa])
+                const double e_ = epf ? lut_s[eps_s[rw * N + aa]]
                                       : (a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
                                                    : __ldg(a.eps_inv + rowofs + aa));
                 const double s_ = a.inv_n * e_;
@@ -195,17 +220,13 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             }
     }
     if (CG) {
-        // per-vector partial of (p, M p); the last CTA of the launch forms alpha
-        const int vec = vl / 3;
-        const int nb = gridDim.x * 3;
-        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         // D is free here (between the x-FFTs) and holds >= blockDim entries
-        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
-        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D)) cg_finish_alpha(cgf, nb, nvec_all, D);
+        const double2 bs = block_sum(make_double2(pmp, 0.0), D);
+        if (tid == 0) acc_s[(vl - a.comp0) / 3] += bs.x;
         __syncthreads();
     }
     BNF_PROBE(6);   // eps (+ CG partial)
-    fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root);
+    fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
     BNF_PROBE(7);   // x-FFT*
     // exchange X -> Y: element (b, a) goes to CTA a / CW, row b, column a % CW (ld CW)
     Cluster<P>::sync_relaxed();
@@ -224,16 +245,14 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         // e^{+2 pi i b M / n12} for b = N2 m + t: w^t (w^N2)^m
         const unsigned Pt = ((unsigned)t * M) % n12;
         const unsigned Pu = ((unsigned)N2 * M) % n12;
-        double2 f = tw_at(a.tw, Pt * s3);
+        const double2 wt = tw_at(a.tw, Pt * s3);
         const double2 wu = tw_at(a.tw, Pu * s3);
 #pragma unroll
-        for (int m = 0; m < N1; ++m) {
-            v[m] = cmul(D[(N2 * m + t) * CW + w], f);
-            f = cmul(f, wu);
-        }
+        for (int m = 0; m < N1; ++m) v[m] = D[(N2 * m + t) * CW + w];
+        fast::twiddle_natural<N1, N2>(v, wt, wu);
     }
     __syncthreads();
-    fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root);
+    fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
     BNF_PROBE(11);  // twiddle* + y-FFT*
 #pragma unroll
     for (int u = 0; u < N1 / N2; ++u)
@@ -243,15 +262,24 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             plane[(size_t)j * N + i] = v[u * N2 + k2];
         }
     BNF_PROBE(12);  // stores issued
-    if (a.prof != nullptr && threadIdx.x == 0) atomicAdd(a.prof + 15, 1ull);   // CTA count
+    if (a.prof != nullptr && threadIdx.x == 0) atomicAdd(a.prof + 15, 1ull);   // plane-part count
+    __syncthreads();   // D is reused by the next plane
+    }   // planes
+    if (CG) {
+        // per-CTA partials of (p, M p) for every vector; the last CTA of the launch forms alpha
+        const int nvec = nslab / 3;
+        const int nb = gridDim.x;
+        if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
+        __syncthreads();
+        if (cg_last_block(cgf.counter + 0, nb, D)) cg_finish_alpha(cgf, nb, nvec, D);
+    }
 }
 
 template <int N1, int N2, int P>
 cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
-    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (size_t)C::CW * C::N;
+    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (size_t)C::CW * C::N + 256 * sizeof(double);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(P * a.mp.n3), (unsigned)nslab, 1);
     cfg.blockDim = dim3(C::NT, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -261,7 +289,8 @@ cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse*
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = P > 1 ? 1 : 0;
+    cfg.numAttrs = 1;
+    const int total = a.mp.n3 * nslab;
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -269,7 +298,22 @@ cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse*
             e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             if (e != cudaSuccess) return e;
         }
-        return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg);
+        // persistent: as many clusters as can be co-resident (cached per kernel)
+        static int ncl_max = 0;
+        if (ncl_max == 0) {
+            cfg.gridDim = dim3((unsigned)(P * total), 1, 1);
+            e = cudaOccupancyMaxActiveClusters(&ncl_max, kern, &cfg);
+            if (e != cudaSuccess || ncl_max < 1) {
+                int dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                ncl_max = std::max(1, nsm / P);
+                (void)cudaGetLastError();
+            }
+        }
+        const int ncl = a.plane_persist ? std::min(total, ncl_max) : total;
+        cfg.gridDim = dim3((unsigned)(P * ncl), 1, 1);
+        return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg, nslab);
     };
     if (cg) return run(k_plane<N1, N2, P, 1>, *cg);
     return run(k_plane<N1, N2, P, 0>, CGFuse{});

@@ -169,7 +169,7 @@ struct bnf_solver {
     cudaStream_t st = nullptr;
     long long n = 0;
     OpArgs args{};
-    DevBuf root[3], twlo, twhi;
+    DevBuf root[3], root2[3], twlo, twhi;
     DevBuf eps_inv, eps_idx, eps_lut;
     bool eps_set = false;
     DevBuf sigma;
@@ -285,6 +285,15 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
         RUN("plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+    } else if (s->l2_slabs) {
+        // y -> x -> y per component slab: the slab stays resident in L2 between the passes
+        OpArgs sa = s->args;
+        for (int vl = 0; vl < 3 * nvec; ++vl) {
+            sa.comp0 = vl;
+            RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
+            RUN("xpass", launch_xpass_slab(sa, U, nullptr, s->st));
+            RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
+        }
     } else {
         RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
@@ -372,6 +381,15 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
         BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
+    } else if (s->l2_slabs) {
+        OpArgs sa = s->args;
+        sa.nvec_all = nvec;
+        for (int vl = 0; vl < 3 * nvec; ++vl) {
+            sa.comp0 = vl;
+            BNF_K(launch_ypass_slab(sa, U, 0, st));
+            BNF_K(launch_xpass_slab(sa, U, &cg, st));
+            BNF_K(launch_ypass_slab(sa, U, 1, st));
+        }
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
@@ -486,6 +504,15 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN("plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+            } else if (s->l2_slabs) {
+                OpArgs sa = s->args;
+                sa.nvec_all = nvec;
+                for (int vl = 0; vl < 3 * nvec; ++vl) {
+                    sa.comp0 = vl;
+                    RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
+                    RUN("xpass_cg", launch_xpass_slab(sa, U, &cg, s->st));
+                    RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
+                }
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
                 RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
@@ -782,6 +809,17 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         CK(s->root[d].ensure(pl.N * sizeof(double2)));
         CK(cudaMemcpy(s->root[d].p, h.data(), pl.N * sizeof(double2), cudaMemcpyHostToDevice));
         pl.root = s->root[d].as<double2>();
+        // fast-plan stage twiddles [k1][t] (N = N1 * N2, fastfft.cuh); same split as the kernels' plans
+        const int n2f = fast_split_N2(pl.N);
+        if (n2f > 0) {
+            const int n1f = pl.N / n2f;
+            std::vector<double2> h2((size_t)n1f * n2f);
+            for (int k1 = 0; k1 < n1f; ++k1)
+                for (int t = 0; t < n2f; ++t) h2[(size_t)k1 * n2f + t] = unit_root((long long)t * k1, pl.N);
+            CK(s->root2[d].ensure(h2.size() * sizeof(double2)));
+            CK(cudaMemcpy(s->root2[d].p, h2.data(), h2.size() * sizeof(double2), cudaMemcpyHostToDevice));
+            pl.root2 = s->root2[d].as<double2>();
+        }
     }
     // two-level table of e^{2 pi i P / n}
     int shift = 0;
@@ -855,6 +893,9 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
     if (const char* cw = std::getenv("BNF_PLANE_CW")) s->args.plane_cw = std::atoi(cw);
+    s->args.plane_persist = std::getenv("BNF_PLANE_PERSIST") ? 1 : 0;
+    s->args.plane_stagger = 0;
+    if (const char* sg = std::getenv("BNF_PLANE_STAGGER")) s->args.plane_stagger = std::atoll(sg);
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

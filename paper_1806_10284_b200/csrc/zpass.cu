@@ -165,24 +165,17 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
         __syncthreads();
-        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
+        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
         const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
         const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
         const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
         const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
         double2* out = U + (size_t)vec * 3 * n + (size_t)l * n + gcol;
-        double2 au = wt;
+        fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
 #pragma unroll
-        for (int u = 0; u < N1 / N2; ++u) {
-            double2 f = au;
+        for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                const int cc = t + N2 * u + N1 * k2;
-                out[kstride * cc] = cmul(v[u * N2 + k2], f);
-                f = cmul(f, wk);
-            }
-            au = cmul(au, wu);
-        }
+            for (int k2 = 0; k2 < N2; ++k2) out[kstride * (t + N2 * u + N1 * k2)] = v[u * N2 + k2];
     }
 }
 
@@ -236,16 +229,14 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
         const int l = tid / (W * N2), t = (tid / W) % N2;
         double2* ct = sm + (size_t)l * TE;
         const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
-        double2 f = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
+        const double2 wt = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
         const double2 wu = conj2(tw_at(a.tw, ((unsigned long long)N2 * N3) % nn));
         double2 v[N1];
 #pragma unroll
-        for (int m = 0; m < N1; ++m) {
-            v[m] = cmul(ct[(N2 * m + t) * W + w], f);
-            f = cmul(f, wu);
-        }
+        for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
+        fast::twiddle_natural<N1, N2>(v, wt, wu);
         __syncthreads();
-        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root);
+        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
