@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--block", type=int, default=2)
     ap.add_argument("--guard", type=int, default=2)
+    ap.add_argument("--warm", type=int, default=1,
+                    help="start each k-point from the previous one's Ritz vectors (DESIGN R17)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -215,7 +217,8 @@ def main():
     eps = eps_for(cfg, lat)
     ks = kappas(cfg, lat)
     stream = torch.cuda.Stream()
-    S = bnf.Solver(lat, device=local, stream=stream.cuda_stream, profile=0, block=args.block, guard=args.guard)
+    S = bnf.Solver(lat, device=local, stream=stream.cuda_stream, profile=0, block=args.block, guard=args.guard,
+                   warm=args.warm)
     S.set_epsilon(eps)
     nev = cfg.nev
 
@@ -353,6 +356,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "grid": list(cfg.n), "nev": nev, "kpoints_on_path": len(ks),
                    "block": args.block, "guard": args.guard, "tol_outer": 1e-12, "tol_inner": 1e-13,
+                   "warm_start": bool(args.warm),
                    "l2": "inputs larger than L2 (Krylov basis and work arrays >> 126 MB)",
                    "parallelism": "k-point replicas x%d" % world},
         "kpoints_per_s": kps,

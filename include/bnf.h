@@ -117,6 +117,8 @@ typedef struct {
     unsigned long long seed;    /* start-block seed (counter-based generator) */
     int refine;                 /* 1: final subspace-iteration + Rayleigh-Ritz on A_r (DESIGN R15) */
     int profile;                /* 1: time every kernel with CUDA events (bnf_kernel_times) */
+    int warm;                   /* 1: start each solve from the previous solve's Ritz vectors
+                                   (neighbouring k on a path; DESIGN R17); 0: seeded random block */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);

@@ -55,12 +55,32 @@ __device__ void cg_block_partial(double v, double* slot, double2* scratch) {
     const double2 s = block_sum(make_double2(v, 0.0), scratch);
     if (threadIdx.x == 0) *slot = s.x;
 }
-__device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2* scratch) {
+// "Last CTA done" election over `total` CTAs with a two-level counter
+// (kCgGroups sub-counters + one top counter, laid out [top][sub...]) so that
+// thousands of CTAs do not serialise on one L2 atomic.  The elected CTA
+// resets all counters (every CTA has arrived by then).
+constexpr int kCgGroups = 64;
+// lin: this CTA's index among the `total` (default: its linear index in the grid;
+// split launches pass their global index)
+__device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2* scratch, long long lin_in = -1) {
     __shared__ int is_last;
     if (threadIdx.x == 0) {
+        const unsigned int lin = lin_in >= 0 ? (unsigned int)lin_in
+                                             : blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        const unsigned int ng = total < (unsigned)kCgGroups ? total : (unsigned)kCgGroups;
+        const unsigned int g = lin % ng;
+        const unsigned int gsize = total / ng + (g < total % ng ? 1u : 0u);
         __threadfence();
-        const unsigned int prev = atomicAdd(counter, 1u);
-        is_last = (prev == total - 1) ? 1 : 0;
+        int last = 0;
+        if (atomicAdd(counter + 1 + g, 1u) == gsize - 1) {
+            __threadfence();
+            last = (atomicAdd(counter, 1u) == ng - 1) ? 1 : 0;
+        }
+        if (last) {
+            counter[0] = 0u;
+            for (unsigned int q = 0; q < ng; ++q) counter[1 + q] = 0u;
+        }
+        is_last = last;
     }
     __syncthreads();
     if (is_last) __threadfence();
@@ -84,7 +104,6 @@ __device__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scr
             cg.alpha[v] = (cg.active[v] && pmp > 0.0) ? cg.rr[v] / pmp : 0.0;
         }
     }
-    if (threadIdx.x == 0) cg.counter[0] = 0u;
 }
 __device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
     for (int v = 0; v < nvec; ++v) {
@@ -97,7 +116,6 @@ __device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scra
         }
     }
     if (threadIdx.x == 0) {
-        cg.counter[1] = 0u;
         // device-side loop control of the CG graph (solver.cu, cg_graph): continue
         // while any vector is active and the iteration cap is not reached
         if (cg.iter != nullptr) {

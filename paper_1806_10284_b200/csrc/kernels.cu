@@ -820,7 +820,8 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
         const int nb = gridDim.x * 3;
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
-        if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm)) cg_finish_alpha(cg, nb, nvec_all, sm);
+        const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
+        if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) cg_finish_alpha(cg, nb, nvec_all, sm);
     }
     fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
     if (ok) {
@@ -1007,7 +1008,7 @@ __global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restr
     if (CG) {
         const int nb = gridDim.x * gridDim.y;
         cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, sm);
-        if (cg_last_block(cg.counter + 1, gridDim.x * gridDim.y * gridDim.z, sm)) cg_finish_beta(cg, nb, gridDim.z, sm);
+        if (cg_last_block(cg.counter + 1 + kCgGroups, gridDim.x * gridDim.y * gridDim.z, sm)) cg_finish_beta(cg, nb, gridDim.z, sm);
     }
 }
 
@@ -1085,6 +1086,13 @@ cudaError_t fast_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaS
     switch (a.mp.n2) {
 #define BNF_CASE(NN, A, B)                                                                                    \
     case NN: {                                                                                                \
+        if (a.yw == 32 && NN >= 32 && A * B * 32 * 16 <= 160 * 1024) {                                       \
+            constexpr int W = 32;                                                                             \
+            dim3 g((a.mp.n1 + W - 1) / W, a.mp.n3, nvec > 0 ? 3 * nvec : 1);                                  \
+            const size_t sm = (size_t)fast::XchW<A, B, W>::size * sizeof(double2);                           \
+            return adjoint ? launch_k(k_ypass_fast<A, B, W, 1>, g, W * B, sm, st, U, a)                       \
+                           : launch_k(k_ypass_fast<A, B, W, 0>, g, W * B, sm, st, U, a);                      \
+        }                                                                                                     \
         constexpr int W = yW();                                                                               \
         dim3 g((a.mp.n1 + W - 1) / W, a.mp.n3, nvec > 0 ? 3 * nvec : 1);                                      \
         const size_t sm = (size_t)fast::XchW<A, B, W>::size * sizeof(double2);                               \

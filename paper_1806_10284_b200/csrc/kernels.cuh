@@ -56,6 +56,7 @@ struct OpArgs {
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
     int plane_cw;            // plane pass: columns per CTA (32 default, 16 = twice the cluster size)
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
+    int yw;                     // y pass columns per CTA (16 default, 32)
     int plane_persist;          // plane pass: persistent clusters (1) or one cluster per plane (0)
     long long plane_stagger;    // plane pass: start delay (cycles) of the second half of the clusters
 };

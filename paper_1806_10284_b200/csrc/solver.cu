@@ -187,6 +187,8 @@ struct bnf_solver {
     bool fused_ok = false;
     bool l2_slabs = false;
     bool use_plane = false;   // fused y/x/y plane pass (plane.cu)
+    bool plane_ok = false;    // plane pass available for this grid
+    bool plane_tuned = false; // autotune_plane done
     bool use_z2 = false;      // cp.async-staged z passes (zpass.cu)
     bool use_graph = true;    // CG loop as a CUDA graph with a device-side while node
     struct CgGraph {
@@ -208,6 +210,7 @@ struct bnf_solver {
     DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
     int nev_last = 0;
+    int prev_want = 0;   // Ritz vectors of the last solve kept in Yv (warm start)
     int* h_flags = nullptr;     // pinned
     double2* h_small = nullptr;  // pinned scratch for small matrices
     size_t h_small_cap = 0;
@@ -302,6 +305,44 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     if (s->use_z2) RUN("zadj2", launch_zadj2(s->args, U, out, nvec, op, nullptr, s->st));
     else RUN("zadj", launch_zadj(s->args, U, out, nvec, op, s->st));
     s->matvecs += nvec;
+    return BNF_OK;
+}
+
+// Pick the real-space middle of the operator (fused cluster plane pass vs
+// separate y / x / y passes) by timing one application of each on scratch
+// vectors (once per solver and block size; env BNF_PLANE / BNF_NO_PLANE force).
+int autotune_plane(bnf_solver* s, int nvec) {
+    if (s->plane_tuned || !s->plane_ok) return BNF_OK;
+    s->plane_tuned = true;
+    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE")) return BNF_OK;
+    const long long N = 2 * s->n;
+    DevBuf y, o;
+    CK(y.ensure((size_t)N * nvec * sizeof(double2)));
+    CK(o.ensure((size_t)N * nvec * sizeof(double2)));
+    CK(cudaMemsetAsync(y.p, 0, (size_t)N * nvec * sizeof(double2), s->st));
+    RUN("fill_random", launch_fill_random(y.as<double2>(), N, nvec, 12345ull, 0, nullptr, s->n, s->st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float best[2] = {0.f, 0.f};
+    const bool prof = s->prof.on;
+    s->prof.on = false;
+    const long long mv0 = s->matvecs;
+    for (int variant = 0; variant < 2; ++variant) {
+        s->use_plane = variant == 1;
+        TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
+        CK(cudaEventRecord(e0, s->st));
+        for (int r = 0; r < 3; ++r) TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));
+        CK(cudaEventRecord(e1, s->st));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&best[variant], e0, e1));
+    }
+    s->matvecs = mv0;
+    s->prof.on = prof;
+    s->use_plane = best[1] < best[0];
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    s->kver++;   // cached CG graphs were built for the other variant
     return BNF_OK;
 }
 
@@ -882,7 +923,8 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     CK(cudaMallocHost((void**)&s->h_flags, 64 * sizeof(int)));
     s->fused_ok = fast_all(s->args) && std::getenv("BNF_NO_FUSED_CG") == nullptr;
     s->l2_slabs = s->fused_ok && std::getenv("BNF_L2_SLABS") != nullptr;
-    s->use_plane = plane_supported(s->args) && std::getenv("BNF_NO_PLANE") == nullptr;
+    s->plane_ok = plane_supported(s->args);
+    s->use_plane = s->plane_ok && std::getenv("BNF_NO_PLANE") == nullptr;
     {
         std::vector<double2> h(n3);
         for (int k = 0; k < n3; ++k) h[k] = unit_root(k, 2LL * n3);
@@ -895,6 +937,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     if (const char* cw = std::getenv("BNF_PLANE_CW")) s->args.plane_cw = std::atoi(cw);
     s->args.plane_persist = std::getenv("BNF_PLANE_PERSIST") ? 1 : 0;
     s->args.plane_stagger = 0;
+    s->args.yw = std::getenv("BNF_YW") ? std::atoi(std::getenv("BNF_YW")) : 16;
     if (const char* sg = std::getenv("BNF_PLANE_STAGGER")) s->args.plane_stagger = std::atoll(sg);
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
@@ -904,7 +947,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->d_iter = s->iterbuf.as<int>();
     if (s->fused_ok) {
         const size_t per = cg_partials_per_vec(s->args);
-        const size_t bytes = 2 * 8 * per * sizeof(double) + 4 * 64 * sizeof(double) + 64;
+        const size_t bytes = 2 * 8 * per * sizeof(double) + 4 * 64 * sizeof(double) + 2 * (1 + 64) * sizeof(unsigned);
         CK(s->cgfuse_buf.ensure(bytes));
         CK(cudaMemset(s->cgfuse_buf.p, 0, bytes));
         char* b = s->cgfuse_buf.as<char>();
@@ -1005,6 +1048,7 @@ int bnf_apply_Ar(bnf_solver* s, const void* y, void* out, int b, int op) {
         set_error("bnf_set_epsilon and bnf_set_kappa must precede bnf_apply_Ar");
         return BNF_ESTATE;
     }
+    TRY(autotune_plane(s, b));
     TRY(apply_op(s, (const double2*)y, (double2*)out, b, op));
     CK(cudaStreamSynchronize(s->st));
     if (s->prof.on) s->prof.flush();
@@ -1027,6 +1071,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     s->graph_calls = 0;
     CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
     TRY(set_kappa_impl(s, kappa));
+    TRY(autotune_plane(s, s->o.block));
     const long long N = 2 * s->n;
     const int b = s->o.block;
     const int want = nev + s->o.guard;
@@ -1044,6 +1089,24 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     double2* W = s->Wb.as<double2>();
     // start block: seeded counter-based normals, Gamma mode masked (R6)
     RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st));
+    if (s->o.warm && s->prev_want > 0) {
+        // Warm start (DESIGN R17): start block = fixed pseudo-random combinations of
+        // the previous solve's Ritz vectors (neighbouring k on the path) plus 1e-3 of
+        // the random block; Gamma mode masked.  Only the start block changes; the
+        // iteration, its tolerance and the returned eigenpairs are as before.
+        const int pw = s->prev_want;
+        std::vector<cd> Wm((size_t)pw * b);
+        unsigned long long h = 0x9E3779B97F4A7C15ull;
+        for (auto& x : Wm) {
+            h ^= h >> 33;
+            h *= 0xff51afd7ed558ccdull;
+            h ^= h >> 33;
+            x = cd(((double)(h >> 11) / 9007199254740992.0) - 0.5, 0.0);
+        }
+        TRY(gemm_nn_host(s, s->Yv.as<double2>(), pw, Wm, b, V, 1.0, 1e-3));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st));
+    }
     bool ok = true;
     std::vector<cd> R0;
     TRY(chol_qr2(s, V, b, R0, ok));
@@ -1207,6 +1270,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     }
     s->lam.assign(lam.begin(), lam.begin() + nev);
     s->nev_last = nev;
+    s->prev_want = want;
     for (int c = 0; c < nev; ++c) lambda[c] = lam[c];
     CK(cudaStreamSynchronize(s->st));
     if (s->prof.on) s->prof.flush();

@@ -277,3 +277,18 @@ def test_graph_cg_equals_eager(bnf):
     assert np.array_equal(l1, l2)
     assert s1["matvecs"] == s2["matvecs"] and s1["inner_iters"] == s2["inner_iters"]
     assert s1["kernel_launches"] > 0 and s2["kernel_launches"] > 0
+
+
+def test_warm_start_same_eigenvalues(bnf):
+    """Warm start (DESIGN R17): starting from the previous k-point's Ritz
+    vectors changes only the start block; the eigenvalues at the next k equal
+    a cold solve's to 1e-10, with no more matvecs."""
+    cfg, n, _ = _cfg_case(4, (32, 32, 32), 0)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape, warm=1)
+    kaps = [tuple(k) for k in cfg.kappa_direct]
+    S.solve(kaps[4], 8)
+    lw, sw = S.solve(kaps[5], 8)
+    _, _, _, Sc = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    lc, sc = Sc.solve(kaps[5], 8)
+    np.testing.assert_allclose(lw, lc, rtol=1e-10)
+    assert sw["matvecs"] <= sc["matvecs"], (sw["matvecs"], sc["matvecs"])
