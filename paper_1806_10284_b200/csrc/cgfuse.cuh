@@ -96,7 +96,7 @@ __device__ double block_sum_fixed(const double* part, int nb, double2* scratch) 
     __syncthreads();
     return res;
 }
-__device__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+__device__ __noinline__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
     for (int v = 0; v < nvec; ++v) {
         const double pmp = block_sum_fixed(cg.part_x + (size_t)v * nb, nb, scratch);
         if (threadIdx.x == 0) {
@@ -105,7 +105,7 @@ __device__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scr
         }
     }
 }
-__device__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
+__device__ __noinline__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
     for (int v = 0; v < nvec; ++v) {
         const double rn = block_sum_fixed(cg.part_z + (size_t)v * nb, nb, scratch);
         if (threadIdx.x == 0) {

@@ -541,15 +541,23 @@ __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restri
         __syncthreads();
         for (int aidx = warp; aidx < p; aidx += 8) {
             const double2* xa = X + (size_t)aidx * N + s0;
-            double2 sum[Q];
+            // two independent accumulator sets (even / odd 32-row groups) for ILP;
+            // their fixed-order combination keeps the result deterministic
+            double2 sum[Q], sum2[Q];
 #pragma unroll
-            for (int c = 0; c < Q; ++c) sum[c] = make_double2(0, 0);
+            for (int c = 0; c < Q; ++c) sum[c] = sum2[c] = make_double2(0, 0);
 #pragma unroll 4
-            for (int r = lane; r < GT_SLICE; r += 32) {
+            for (int r = lane; r < GT_SLICE; r += 64) {
                 const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
+                const double2 x2 = (s0 + r + 32 < N) ? xa[r + 32] : make_double2(0, 0);
 #pragma unroll
-                for (int c = 0; c < Q; ++c) sum[c] = cadd(sum[c], cjmul(x, ys[c * GT_SLICE + r]));
+                for (int c = 0; c < Q; ++c) {
+                    sum[c] = cadd(sum[c], cjmul(x, ys[c * GT_SLICE + r]));
+                    sum2[c] = cadd(sum2[c], cjmul(x2, ys[c * GT_SLICE + r + 32]));
+                }
             }
+#pragma unroll
+            for (int c = 0; c < Q; ++c) sum[c] = cadd(sum[c], sum2[c]);
 #pragma unroll
             for (int c = 0; c < Q; ++c) {
                 if (c < q) {
@@ -564,6 +572,9 @@ __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restri
 }
 
 // Y_c = beta Y_c + alpha sum_a X_a H[a*q + c]   (H on device, p*q <= 4096)
+// Q >= q output columns held in registers; the loop over the p input columns
+// is unrolled by 4 so that four independent 16-byte loads are in flight.
+template <int Q>
 __global__ void __launch_bounds__(256) k_gemm_nn(const double2* X, int p, const double2* __restrict__ H,
                                                  int q, double2* Y, long long N, double alpha,
                                                  double beta) {
@@ -571,18 +582,32 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double2* X, int p, const 
     for (int t = threadIdx.x; t < p * q; t += blockDim.x) hs[t] = H[t];
     __syncthreads();
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < N; r += (long long)gridDim.x * blockDim.x) {
-        double2 acc[8];
+        double2 acc[Q];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = make_double2(0, 0);
-        for (int aidx = 0; aidx < p; ++aidx) {
+        for (int c = 0; c < Q; ++c) acc[c] = make_double2(0, 0);
+        int aidx = 0;
+        for (; aidx + 4 <= p; aidx += 4) {
+            double2 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = X[(size_t)(aidx + u) * N + r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int c = 0; c < Q; ++c)
+                    if (c < q) acc[c] = cadd(acc[c], cmul(x[u], hs[(aidx + u) * q + c]));
+        }
+        for (; aidx < p; ++aidx) {
             const double2 x = X[(size_t)aidx * N + r];
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
+            for (int c = 0; c < Q; ++c)
                 if (c < q) acc[c] = cadd(acc[c], cmul(x, hs[aidx * q + c]));
         }
-        for (int c = 0; c < q; ++c) {
-            double2 y = (beta == 0.0) ? make_double2(0, 0) : cscale(Y[(size_t)c * N + r], beta);
-            Y[(size_t)c * N + r] = cadd(y, cscale(acc[c], alpha));
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+            if (c < q) {
+                const double2 y = (beta == 0.0) ? make_double2(0, 0) : cscale(Y[(size_t)c * N + r], beta);
+                Y[(size_t)c * N + r] = cadd(y, cscale(acc[c], alpha));
+            }
         }
     }
 }
@@ -815,18 +840,20 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
             if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);      // (p, M p) = sum |T v|^2 / eps
             v[u * N2 + k2] = cscale(x, s_);
         }
+    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
+    if (ok) {
+#pragma unroll
+        for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
+    }
     if (CG) {
+        // (p, M p) partial of this CTA, reduced after the stores are issued; the
+        // last CTA of the launch forms alpha (read by the next pass, zadj)
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
         if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) cg_finish_alpha(cg, nb, nvec_all, sm);
-    }
-    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
-    if (ok) {
-#pragma unroll
-        for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
     }
 }
 
@@ -1236,9 +1263,17 @@ cudaError_t launch_gemm_tn_final(const double2* partial, int nblk, int pq, doubl
 cudaError_t launch_gemm_nn(const double2* X, int p, const double2* H, int q, double2* Y, long long N, double alpha,
                            double beta, cudaStream_t st) {
     const size_t sm = (size_t)p * q * sizeof(double2);
-    cudaError_t e = set_smem((const void*)k_gemm_nn, sm);
+    if (q > 8) return cudaErrorInvalidValue;
+    const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
+    const void* f = Q == 1 ? (const void*)k_gemm_nn<1> : Q == 2 ? (const void*)k_gemm_nn<2>
+                  : Q == 4 ? (const void*)k_gemm_nn<4> : (const void*)k_gemm_nn<8>;
+    cudaError_t e = set_smem(f, sm);
     if (e != cudaSuccess) return e;
-    k_gemm_nn<<<grid_for(N, 256), 256, sm, st>>>(X, p, H, q, Y, N, alpha, beta);
+    const int g = grid_for(N, 256);
+    if (Q == 1) k_gemm_nn<1><<<g, 256, sm, st>>>(X, p, H, q, Y, N, alpha, beta);
+    else if (Q == 2) k_gemm_nn<2><<<g, 256, sm, st>>>(X, p, H, q, Y, N, alpha, beta);
+    else if (Q == 4) k_gemm_nn<4><<<g, 256, sm, st>>>(X, p, H, q, Y, N, alpha, beta);
+    else k_gemm_nn<8><<<g, 256, sm, st>>>(X, p, H, q, Y, N, alpha, beta);
     return cudaGetLastError();
 }
 

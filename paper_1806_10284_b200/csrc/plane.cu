@@ -219,12 +219,6 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
                 v[u * N2 + k2] = cscale(x, s_);
             }
     }
-    if (CG) {
-        // D is free here (between the x-FFTs) and holds >= blockDim entries
-        const double2 bs = block_sum(make_double2(pmp, 0.0), D);
-        if (tid == 0) acc_s[(vl - a.comp0) / 3] += bs.x;
-        __syncthreads();
-    }
     BNF_PROBE(6);   // eps (+ CG partial)
     fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
     BNF_PROBE(7);   // x-FFT*
@@ -263,6 +257,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         }
     BNF_PROBE(12);  // stores issued
     if (a.prof != nullptr && threadIdx.x == 0) atomicAdd(a.prof + 15, 1ull);   // plane-part count
+    if (CG) {
+        // this plane's (p, M p) partial (D is free after the y-FFT*; >= blockDim entries)
+        const double2 bs = block_sum(make_double2(pmp, 0.0), D);
+        if (tid == 0) acc_s[(vl - a.comp0) / 3] += bs.x;
+    }
     __syncthreads();   // D is reused by the next plane
     }   // planes
     if (CG) {

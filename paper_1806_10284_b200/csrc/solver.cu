@@ -938,6 +938,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.plane_persist = std::getenv("BNF_PLANE_PERSIST") ? 1 : 0;
     s->args.plane_stagger = 0;
     s->args.yw = std::getenv("BNF_YW") ? std::atoi(std::getenv("BNF_YW")) : 16;
+    s->args.zunroll = std::getenv("BNF_Z_UNROLL") ? std::atoi(std::getenv("BNF_Z_UNROLL")) : 1;
     if (const char* sg = std::getenv("BNF_PLANE_STAGGER")) s->args.plane_stagger = std::atoll(sg);
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
