@@ -541,23 +541,15 @@ __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restri
         __syncthreads();
         for (int aidx = warp; aidx < p; aidx += 8) {
             const double2* xa = X + (size_t)aidx * N + s0;
-            // two independent accumulator sets (even / odd 32-row groups) for ILP;
-            // their fixed-order combination keeps the result deterministic
-            double2 sum[Q], sum2[Q];
+            double2 sum[Q];
 #pragma unroll
-            for (int c = 0; c < Q; ++c) sum[c] = sum2[c] = make_double2(0, 0);
+            for (int c = 0; c < Q; ++c) sum[c] = make_double2(0, 0);
 #pragma unroll 4
-            for (int r = lane; r < GT_SLICE; r += 64) {
+            for (int r = lane; r < GT_SLICE; r += 32) {
                 const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
-                const double2 x2 = (s0 + r + 32 < N) ? xa[r + 32] : make_double2(0, 0);
 #pragma unroll
-                for (int c = 0; c < Q; ++c) {
-                    sum[c] = cadd(sum[c], cjmul(x, ys[c * GT_SLICE + r]));
-                    sum2[c] = cadd(sum2[c], cjmul(x2, ys[c * GT_SLICE + r + 32]));
-                }
+                for (int c = 0; c < Q; ++c) sum[c] = cadd(sum[c], cjmul(x, ys[c * GT_SLICE + r]));
             }
-#pragma unroll
-            for (int c = 0; c < Q; ++c) sum[c] = cadd(sum[c], sum2[c]);
 #pragma unroll
             for (int c = 0; c < Q; ++c) {
                 if (c < q) {
@@ -840,20 +832,20 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
             if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);      // (p, M p) = sum |T v|^2 / eps
             v[u * N2 + k2] = cscale(x, s_);
         }
-    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
-    if (ok) {
-#pragma unroll
-        for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
-    }
     if (CG) {
-        // (p, M p) partial of this CTA, reduced after the stores are issued; the
-        // last CTA of the launch forms alpha (read by the next pass, zadj)
+        // (p, M p) partial of this CTA; the last CTA of the launch forms alpha
+        // (read by the next pass, zadj)
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
         if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) cg_finish_alpha(cg, nb, nvec_all, sm);
+    }
+    fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
+    if (ok) {
+#pragma unroll
+        for (int m = 0; m < N1; ++m) row[N2 * m + t] = v[m];
     }
 }
 

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--kidx", default="5,12")
     ap.add_argument("--settings", default="1:2,2:2,2:4,4:2,4:4")
     ap.add_argument("--refine", type=int, default=1)
+    ap.add_argument("--warm", type=int, default=0)
     args = ap.parse_args()
     cfg = configs.config(args.config)
     lat = bnf.Lattice(cfg.a_raw, cfg.n)
@@ -35,7 +36,7 @@ def main():
     ref = {}
     for st in args.settings.split(","):
         b, g = (int(x) for x in st.split(":"))
-        S = bnf.Solver(lat, block=b, guard=g, refine=args.refine)
+        S = bnf.Solver(lat, block=b, guard=g, refine=args.refine, warm=args.warm)
         S.set_epsilon(eps)
         for ki in (int(x) for x in args.kidx.split(",")):
             torch.cuda.synchronize()

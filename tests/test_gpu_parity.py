@@ -292,3 +292,57 @@ def test_warm_start_same_eigenvalues(bnf):
     lc, sc = Sc.solve(kaps[5], 8)
     np.testing.assert_allclose(lw, lc, rtol=1e-10)
     assert sw["matvecs"] <= sc["matvecs"], (sw["matvecs"], sc["matvecs"])
+
+
+def test_kpath_solve_path_matches_direct(bnf, tmp_path):
+    """kpath.solve_path (the k-path scheduler, single process) returns, in path
+    order, the same eigenvalues as direct solves; a resumed run reuses the
+    checkpoint."""
+    from paper_1806_10284_b200 import kpath
+    cfg = configs.config(3)
+    n = (12, 12, 9)
+    O = olat.snap(cfg.a_raw, n)
+    eps = E.stacked(E.sample(cfg.shape, n, O.a, O.delta, O.a_canon))
+    kaps = [tuple(olat.kvec_reduce(O, K)) for K in cfg.kpoints[:4]]
+    recs = kpath.solve_path(cfg.a_raw, n, eps, kaps, 6, device=0, checkpoint_dir=str(tmp_path))
+    assert [r.index for r in recs] == [0, 1, 2, 3] and all(r.status == "ok" for r in recs)
+    L = bnf.Lattice(cfg.a_raw, n)
+    S = bnf.Solver(L)
+    S.set_epsilon(eps)
+    for r in recs:
+        lam, _ = S.solve(r.kappa, 6)
+        np.testing.assert_allclose(r.lam, lam, rtol=1e-10)
+    again = kpath.solve_path(cfg.a_raw, n, eps, kaps, 6, device=0, checkpoint_dir=str(tmp_path))
+    assert [r.lam for r in again] == [r.lam for r in recs]
+
+
+def test_anisotropic_fast_path_vs_oracle(bnf):
+    """A non-cubic grid on the production fast path (z passes with W = 16,
+    separate y / x passes since n1 != n2): A_r and M vs the oracle operator."""
+    cfg = configs.config(4)
+    n = (48, 32, 64)
+    O = olat.snap(cfg.a_raw, n)
+    kap = olat.kappa_from_raw(O, cfg.kappa_direct[7])
+    L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    op = fftop.NFSEPOperator(O, kap, eps)
+    y = vectors.complex_normal((2, 2 * O.nn), seed=21)
+    for code, name in ((bnf.OP_AR, "Ar"), (bnf.OP_M, "M")):
+        got = _apply_gpu(S, kap, y, code)
+        for v in range(2):
+            want = op.apply(y[v], name)
+            assert np.abs(got[v] - want).max() <= OP_TOL * np.abs(want).max()
+
+
+def test_plane_and_yxy_middles_agree(bnf, monkeypatch):
+    """The fused cluster plane pass and the separate y / x / y passes compute
+    the same operator (same FFT arithmetic): equal to rounding."""
+    cfg, n, kap = _cfg_case(2)
+    outs = []
+    for env in ("BNF_PLANE", "BNF_NO_PLANE"):
+        monkeypatch.setenv(env, "1")
+        L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
+        y = vectors.complex_normal((2, 2 * O.nn), seed=22)
+        outs.append(_apply_gpu(S, kap, y, bnf.OP_AR))
+        S.close()
+        monkeypatch.delenv(env)
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-13 * np.abs(outs[1]).max()
