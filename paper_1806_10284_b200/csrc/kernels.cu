@@ -517,15 +517,15 @@ __global__ void __launch_bounds__(256) k_sum_final(const double2* __restrict__ p
 }
 
 // Tall-skinny X^* Y: X has p vectors, Y has q <= Q vectors, length N.
-// Block = 8 warps over a slice of GT_SLICE rows (grid-stride over slices).
+// Block = 8 warps over a slice of GT_SLICE = 512 rows (grid-stride over slices).
 // The Y slice is staged in shared memory; warp w owns the columns a = w mod 8
 // of X, streams X_a over the slice and accumulates into acc[a][c] (owned
 // exclusively by that warp -> deterministic, no atomics).  partial[(a*q+c)*nblk + blk].
-constexpr int GT_SLICE = 512;
 template <int Q>
 __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restrict__ X, int p,
                                                          const double2* __restrict__ Y, int q, long long N,
                                                          double2* __restrict__ partial) {
+    constexpr int GT_SLICE = 512;   // rows per slice
     extern __shared__ double2 gsm[];
     double2* ys = gsm;                       // [Q][GT_SLICE]
     double2* acc = gsm + Q * GT_SLICE;       // [p][q]
@@ -1235,7 +1235,8 @@ cudaError_t launch_gemm_tn_partial(const double2* X, int p, const double2* Y, in
                                    int nblk, cudaStream_t st) {
     const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
     if (q > 8) return cudaErrorInvalidValue;
-    const size_t sm = ((size_t)Q * GT_SLICE + (size_t)p * q) * sizeof(double2);
+    const int slice = 512;
+    const size_t sm = ((size_t)Q * slice + (size_t)p * q) * sizeof(double2);
     const void* f = Q == 1 ? (const void*)k_gemm_tn_partial<1> : Q == 2 ? (const void*)k_gemm_tn_partial<2>
                   : Q == 4 ? (const void*)k_gemm_tn_partial<4> : (const void*)k_gemm_tn_partial<8>;
     cudaError_t e = set_smem(f, sm);

@@ -1,0 +1,75 @@
+"""Full band paths of the BASELINE configs through the k-path scheduler
+(kpath.solve_path): wall time and k-points/s per config, eigenvalue
+agreement with the oracle goldens where they exist (tests/golden/full_c*),
+and the a-posteriori residual of every k-point.
+
+    python scripts/path_bench.py [--configs 1,2,3,4,5] [--out profiles/r01_paths.json]
+"""
+import argparse
+import glob
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1806_10284_b200 as bnf  # noqa: E402
+from paper_1806_10284_b200 import kpath  # noqa: E402
+from bench import eps_for, kappas  # noqa: E402
+from synthetic import configs  # noqa: E402
+
+
+def goldens():
+    out = {}
+    for f in glob.glob(os.path.join(ROOT, "tests", "golden", "full_c*_oracle.json")):
+        with open(f) as fh:
+            g = json.load(fh)
+        out[(g["config"], tuple(round(x, 12) for x in g["kappa"]))] = g["lambda"]
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--warm", type=int, default=1)
+    a = ap.parse_args()
+    gold = goldens()
+    res = []
+    for idx in [int(x) for x in a.configs.split(",")]:
+        cfg = configs.config(idx)
+        lat = bnf.Lattice(cfg.a_raw, cfg.n)
+        eps = eps_for(cfg, lat)
+        ks = kappas(cfg, lat)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        dev = []
+        for r in recs:
+            key = (idx, tuple(round(x, 12) for x in r.kappa))
+            if key in gold:
+                g = np.asarray(gold[key][:len(r.lam)])
+                dev.append(float(np.max(np.abs(np.asarray(r.lam[:len(g)]) - g) / g)))
+        line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
+                "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
+                "matvecs_per_kpoint": float(np.mean([r.stats["matvecs"] for r in recs])),
+                "max_residual": max(r.stats["max_residual"] for r in recs),
+                "golden_kpoints": len(dev), "max_rel_dev_vs_oracle": max(dev) if dev else None,
+                "lambda_first_k": recs[0].lam[:4], "omega_over_2pi_first_k": kpath.frequencies(recs[0].lam[:4])}
+        print(json.dumps(line), flush=True)
+        res.append(line)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
