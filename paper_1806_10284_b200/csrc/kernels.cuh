@@ -58,6 +58,7 @@ struct OpArgs {
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
     int yw;                     // y pass columns per CTA (16 default, 32)
     int zunroll;                // z passes: elements per thread processed together in the mode loops (1, 2)
+    int plane_l2;               // plane pass: one CTA per plane, strips exchanged through L2 (1) or cluster/DSMEM (0)
     int plane_persist;          // plane pass: persistent clusters (1) or one cluster per plane (0)
     long long plane_stagger;    // plane pass: start delay (cycles) of the second half of the clusters
 };

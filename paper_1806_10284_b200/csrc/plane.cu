@@ -274,6 +274,126 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     }
 }
 
+// ---------------------------------------------------------------------------
+// L2 variant: one CTA per (component, z-plane).  The CTA runs the P column
+// strips of phase Y, then the P row strips of phase X, then the P column
+// strips of phase Y* one after the other (each strip = one cluster rank's
+// work above), exchanging the strips through the plane itself in global
+// memory: the plane (N*N*16 B, 256 KB at 128^2) is re-read while it is hot
+// in L2, so DRAM still sees one read and one write per element, and there
+// are no cluster barriers or DSMEM stores.  Two CTAs per SM overlap.
+template <int N1, int N2, int P, int CG>
+__global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
+    using C = PlaneCfg<N1, N2, P>;
+    constexpr int N = C::N, CW = C::CW;
+    extern __shared__ double2 D[];
+    const ModeP& p = a.mp;
+    const int tid = threadIdx.x;
+    const int c = blockIdx.x;
+    const int vl = blockIdx.y + a.comp0;
+    const int l = vl % 3;
+    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    constexpr bool EPF = (N % 16) == 0;
+    unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);   // [N][N] material indices
+    double* lut_s = reinterpret_cast<double*>(eps_s + N * N);
+    const bool epf = EPF && a.eps_idx != nullptr;
+    if (epf) {
+        for (int q = tid; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
+        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c;
+        for (int q = tid; q < N * N / 16; q += C::NT) cp_async16(eps_s + 16 * q, src + 16 * q);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    const int w = tid % CW, t = tid / CW;          // strip-column layout (phases Y, Y*)
+    const int tx = tid % N2, rw = tid / N2;        // strip-row layout (phase X)
+    const unsigned n12 = (unsigned)p.n12;
+    const unsigned long long s3 = (unsigned long long)p.n3;
+    double2 v[N1];
+    // ---------------- phase Y: column strips ----------------
+    for (int r = 0; r < P; ++r) {
+        const int i = r * CW + w;
+        const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
+        const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
+        const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
+        const double2 wk = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3));
+        fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+    }
+    if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();   // the strips written above are read by other threads below (block scope)
+    // ---------------- phase X: row strips ----------------
+    double pmp = 0.0;
+    for (int r = 0; r < P; ++r) {
+        const int b = r * CW + rw;
+        double2* row = plane + (size_t)b * N;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + tx];
+        fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
+        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int aa = tx + N2 * u + N1 * k2;
+                const double e_ = epf ? lut_s[eps_s[b * N + aa]]
+                                      : (a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
+                                                   : __ldg(a.eps_inv + rowofs + aa));
+                const double s_ = a.inv_n * e_;
+                const double2 x = v[u * N2 + k2];
+                if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
+                v[u * N2 + k2] = cscale(x, s_);
+            }
+        fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) row[N2 * m + tx] = v[m];
+    }
+    __syncthreads();
+    // ---------------- phase Y*: column strips ----------------
+    for (int r = 0; r < P; ++r) {
+        const int i = r * CW + w;
+        const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
+        const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
+        fast::twiddle_natural<N1, N2>(v, wt, wu);
+        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+    }
+    if (CG) {
+        // this plane's (p, M p) partial; the last CTA of the launch forms alpha
+        const int vec = vl / 3;
+        const int nb = gridDim.x * 3;
+        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
+        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        const long long lin = (long long)vl * gridDim.x + blockIdx.x;
+        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D, lin)) cg_finish_alpha(cgf, nb, nvec_all, D);
+    }
+}
+
+template <int N1, int N2, int P>
+cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    using C = PlaneCfg<N1, N2, P>;
+    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (size_t)C::N * C::N + 256 * sizeof(double);
+    const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
+    auto run = [&](auto kern, auto cgarg) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<g, C::NT, smem, st>>>(U, a, cgarg);
+        return cudaGetLastError();
+    };
+    if (cg) return run(k_plane_l2<N1, N2, P, 1>, *cg);
+    return run(k_plane_l2<N1, N2, P, 0>, CGFuse{});
+}
+
 template <int N1, int N2, int P>
 cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
@@ -336,6 +456,16 @@ bool plane_supported(const OpArgs& a) {
 }
 
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    if (a.plane_l2) {   // one CTA per plane, strips exchanged through L2
+        switch (a.mp.n1) {
+            case 64: return launch_plane_l2_t<8, 8, 2>(a, U, nslab, cg, st);
+            case 96: return launch_plane_l2_t<24, 4, 3>(a, U, nslab, cg, st);
+            case 128: return launch_plane_l2_t<16, 8, 4>(a, U, nslab, cg, st);
+            case 192: return launch_plane_l2_t<24, 8, 6>(a, U, nslab, cg, st);
+            case 256: return launch_plane_l2_t<16, 16, 8>(a, U, nslab, cg, st);
+            default: break;
+        }
+    }
     if (a.plane_cw == 64 && a.mp.n1 == 128) return launch_plane_t<16, 8, 2>(a, U, nslab, cg, st);
     if (a.plane_cw == 16) {   // 16 columns per CTA: smaller CTAs, twice the cluster size
         switch (a.mp.n1) {

@@ -314,7 +314,10 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
 int autotune_plane(bnf_solver* s, int nvec) {
     if (s->plane_tuned || !s->plane_ok) return BNF_OK;
     s->plane_tuned = true;
-    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE")) return BNF_OK;
+    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE")) {
+        s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? 1 : 0;
+        return BNF_OK;
+    }
     const long long N = 2 * s->n;
     DevBuf y, o;
     CK(y.ensure((size_t)N * nvec * sizeof(double2)));
@@ -324,12 +327,14 @@ int autotune_plane(bnf_solver* s, int nvec) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    float best[2] = {0.f, 0.f};
+    // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2
+    float best[3] = {0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;
-    for (int variant = 0; variant < 2; ++variant) {
-        s->use_plane = variant == 1;
+    for (int variant = 0; variant < 3; ++variant) {
+        s->use_plane = variant >= 1;
+        s->args.plane_l2 = variant == 2 ? 1 : 0;
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
         CK(cudaEventRecord(e0, s->st));
         for (int r = 0; r < 3; ++r) TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));
@@ -337,9 +342,13 @@ int autotune_plane(bnf_solver* s, int nvec) {
         CK(cudaEventSynchronize(e1));
         CK(cudaEventElapsedTime(&best[variant], e0, e1));
     }
+    int pick = 0;
+    for (int variant = 1; variant < 3; ++variant)
+        if (best[variant] < best[pick]) pick = variant;
+    s->use_plane = pick >= 1;
+    s->args.plane_l2 = pick == 2 ? 1 : 0;
     s->matvecs = mv0;
     s->prof.on = prof;
-    s->use_plane = best[1] < best[0];
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     s->kver++;   // cached CG graphs were built for the other variant

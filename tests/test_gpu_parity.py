@@ -334,15 +334,37 @@ def test_anisotropic_fast_path_vs_oracle(bnf):
 
 
 def test_plane_and_yxy_middles_agree(bnf, monkeypatch):
-    """The fused cluster plane pass and the separate y / x / y passes compute
-    the same operator (same FFT arithmetic): equal to rounding."""
+    """The three real-space middles -- fused cluster plane pass, plane pass
+    through L2, separate y / x / y passes -- compute the same operator (same FFT
+    arithmetic): equal to rounding, and to the oracle."""
     cfg, n, kap = _cfg_case(2)
     outs = []
-    for env in ("BNF_PLANE", "BNF_NO_PLANE"):
-        monkeypatch.setenv(env, "1")
+    for envs in ({"BNF_PLANE": "1"}, {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"}, {"BNF_NO_PLANE": "1"}):
+        for k, v in envs.items():
+            monkeypatch.setenv(k, v)
         L, O, eps, S = _setup(bnf, cfg.a_raw, n, cfg.shape)
         y = vectors.complex_normal((2, 2 * O.nn), seed=22)
         outs.append(_apply_gpu(S, kap, y, bnf.OP_AR))
         S.close()
-        monkeypatch.delenv(env)
-    assert np.abs(outs[0] - outs[1]).max() <= 1e-13 * np.abs(outs[1]).max()
+        for k in envs:
+            monkeypatch.delenv(k)
+    for o in outs[:2]:
+        assert np.abs(o - outs[2]).max() <= 1e-13 * np.abs(outs[2]).max()
+    op = fftop.NFSEPOperator(O, kap, eps)
+    want = op.apply(y[0], "Ar")
+    assert np.abs(outs[1][0] - want).max() <= OP_TOL * np.abs(want).max()
+
+
+def test_plane_l2_cg_solve(bnf, monkeypatch):
+    """CG-fused solve with the L2 plane middle at full 64^3 (config 2) equals
+    the oracle golden to 1e-10."""
+    monkeypatch.setenv("BNF_PLANE", "1")
+    monkeypatch.setenv("BNF_PLANE_L2", "1")
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full_c2_k9_oracle.json")) as f:
+        g = json.load(f)
+    cfg = configs.config(2)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape)
+    lam, _ = S.solve(tuple(g["kappa"]), len(g["lambda"]))
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
