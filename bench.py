@@ -50,6 +50,8 @@ PASS_BYTES = {
     # fused y/x/y plane pass (plane.cu): one read + write of U, eps as uint8
     "plane": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     "plane_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    "plane_l2": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,     # same bytes, strips exchanged through L2
+    "plane_l2_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     # persistent pipelined z passes (zpass.cu); CG x update deferred into zfwd2_cg
     "zfwd2": lambda n: 2 * 16 * n + 3 * 16 * n,
     "zadj2": lambda n: 3 * 16 * n + 2 * 16 * n,
@@ -346,7 +348,7 @@ def main():
     matvec_ms = sum(v[0] for k, v in ktimes.items() if k in PASS_BYTES)
     matvec_bytes = sum(PASS_BYTES[k](n) * vecs(k) for k in ktimes if k in PASS_BYTES)
     cpu = None
-    if not args.no_cpu and world >= 1:
+    if not args.no_cpu and world == 1:   # the oracle baseline is timed at N = 1 only
         r, c, dt, co = oracle_rate(cfg)
         cpu = {"value": r, "unit": "matvecs/s", "cores": round(co, 2), "kind": "oracle",
                "sample": "%d oracle A_r applications at %s, k-point 1 (numpy FFT, %.1f s)" % (c, cfg.name, dt)}
@@ -373,6 +375,8 @@ def main():
                    "converged": all(s_["converged"] for s_ in stats),
                    "max_residual": max(s_["max_residual"] for s_ in stats)},
         "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
+        "middle": ("plane_l2" if "plane_l2_cg" in ktimes else "plane_cluster" if "plane_cg" in ktimes
+                   else "y/x/y"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -287,7 +287,7 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     if (s->use_z2) RUN("zfwd2", launch_zfwd2(s->args, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
-        RUN("plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+        RUN(s->args.plane_l2 ? "plane_l2" : "plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
     } else if (s->l2_slabs) {
         // y -> x -> y per component slab: the slab stays resident in L2 between the passes
         OpArgs sa = s->args;
@@ -315,7 +315,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
     if (s->plane_tuned || !s->plane_ok) return BNF_OK;
     s->plane_tuned = true;
     if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE")) {
-        s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? 1 : 0;
+        s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? std::atoi(std::getenv("BNF_PLANE_L2")) : 0;
         return BNF_OK;
     }
     const long long N = 2 * s->n;
@@ -553,7 +553,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
-                RUN("plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+                RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
             } else if (s->l2_slabs) {
                 OpArgs sa = s->args;
                 sa.nvec_all = nvec;

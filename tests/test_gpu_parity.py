@@ -334,8 +334,8 @@ def test_anisotropic_fast_path_vs_oracle(bnf):
 
 
 def test_plane_and_yxy_middles_agree(bnf, monkeypatch):
-    """The three real-space middles -- fused cluster plane pass, plane pass
-    through L2, separate y / x / y passes -- compute the same operator (same FFT
+    """The real-space middles -- fused cluster plane pass, plane pass through
+    L2, separate y / x / y passes -- compute the same operator (same FFT
     arithmetic): equal to rounding, and to the oracle."""
     cfg, n, kap = _cfg_case(2)
     outs = []
