@@ -840,7 +840,11 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
-        if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) cg_finish_alpha(cg, nb, nvec_all, sm);
+        if (cg.ext) {
+            if (lin == 0 && threadIdx.x == 0) *cg.nb_x = nb;
+        } else if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) {
+            cg_finish_alpha(cg, nb, nvec_all, sm);
+        }
     }
     fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
     if (ok) {
@@ -1027,8 +1031,21 @@ __global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restr
     if (CG) {
         const int nb = gridDim.x * gridDim.y;
         cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, sm);
-        if (cg_last_block(cg.counter + 1 + kCgGroups, gridDim.x * gridDim.y * gridDim.z, sm)) cg_finish_beta(cg, nb, gridDim.z, sm);
+        if (cg.ext) {
+            if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *cg.nb_z = nb;
+        } else if (cg_last_block(cg.counter + 1 + kCgGroups, gridDim.x * gridDim.y * gridDim.z, sm)) {
+            cg_finish_beta(cg, nb, gridDim.z, sm);
+        }
     }
+}
+
+// CG scalars from the per-CTA partials of the preceding pass (one CTA, fixed
+// summation order): the kernel boundary orders the partials, so the passes
+// need no fences or atomics.
+__global__ void __launch_bounds__(1024) k_cg_finish(CGFuse cg, int which, int nvec) {
+    __shared__ double2 red[32];
+    if (which == 0) cg_finish_alpha(cg, *cg.nb_x, nvec, red);
+    else cg_finish_beta(cg, *cg.nb_z, nvec, red);
 }
 
 inline int grid_for(long long total, int threads, int cap = 148 * 16) {
@@ -1318,6 +1335,11 @@ int fast_split_N2(int N) {
 #undef BNF_CASE
         default: return 0;
     }
+}
+
+cudaError_t launch_cg_finish(const CGFuse& cg, int which, int nvec, cudaStream_t st) {
+    k_cg_finish<<<1, 1024, 0, st>>>(cg, which, nvec);
+    return cudaGetLastError();
 }
 
 bool fast_all(const OpArgs& a) { return a.fast && has_fast(a.mp.n1) && has_fast(a.mp.n2) && has_fast(a.mp.n3); }

@@ -80,6 +80,9 @@ struct CGFuse {
     double* beta;
     double* thr;
     int* active;
+    int* nb_x;                         // partial counts per vector written by the producing passes
+    int* nb_z;                         //   (ext mode: reduced by k_cg_finish after the pass)
+    int ext;                           // 1: scalars formed by k_cg_finish (no in-kernel last-CTA election)
     int* iter;                         // CG iterations done (device), or null
     int max_iter;
     int use_cond;                      // 1: set the CG graph's while-condition
@@ -123,6 +126,9 @@ cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec
                          const CGFuse* cg, cudaStream_t st);
 cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,
                          cudaStream_t st);
+// alpha (which = 0, after the (p, M p) pass) or beta + convergence flags +
+// graph condition (which = 1, after zadj) from the per-CTA partials (one CTA)
+cudaError_t launch_cg_finish(const CGFuse& cg, int which, int nvec, cudaStream_t st);
 cudaError_t launch_cg_xfinal(double2* X, const double2* P, const double* alpha, long long N, int nvec, cudaStream_t st);
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st);
 

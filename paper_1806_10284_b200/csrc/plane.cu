@@ -270,7 +270,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int nb = gridDim.x;
         if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
         __syncthreads();
-        if (cg_last_block(cgf.counter + 0, nb, D)) cg_finish_alpha(cgf, nb, nvec, D);
+        if (cgf.ext) {
+            if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;
+        } else if (cg_last_block(cgf.counter + 0, nb, D)) {
+            cg_finish_alpha(cgf, nb, nvec, D);
+        }
     }
 }
 
@@ -375,7 +379,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D, lin)) cg_finish_alpha(cgf, nb, nvec_all, D);
+        if (cgf.ext) {
+            if (lin == 0 && tid == 0) *cgf.nb_x = nb;
+        } else if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D, lin)) {
+            cg_finish_alpha(cgf, nb, nvec_all, D);
+        }
     }
 }
 

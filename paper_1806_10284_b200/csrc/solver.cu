@@ -431,6 +431,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
         BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else if (s->l2_slabs) {
         OpArgs sa = s->args;
         sa.nvec_all = nvec;
@@ -440,13 +441,16 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
             BNF_K(launch_xpass_slab(sa, U, &cg, st));
             BNF_K(launch_ypass_slab(sa, U, 1, st));
         }
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
         BNF_K(launch_ypass(s->args, U, nvec, 1, st));
     }
     if (s->use_z2) BNF_K(launch_zadj2(s->args, U, R, nvec, 1, &cg, st));
     else BNF_K(launch_zadj_cg(s->args, U, X, nvec, cg, st));
+    BNF_K(launch_cg_finish(cg, 1, nvec, st));
 #undef BNF_K
     *nk = k;
     return cudaSuccess;
@@ -535,6 +539,9 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     CGFuse cg = s->cgf;
     cg.P = P;
     cg.R = R;
+    cg.ext = 1;   // CG scalars by k_cg_finish after each reducing pass
+    cg.nb_x = s->d_iter + 4;
+    cg.nb_z = s->d_iter + 5;
     int it = 0;
     if (!s->prof.on && s->use_graph) {
         cg.iter = s->d_iter;
@@ -554,6 +561,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else if (s->l2_slabs) {
                 OpArgs sa = s->args;
                 sa.nvec_all = nvec;
@@ -563,13 +571,16 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
                     RUN("xpass_cg", launch_xpass_slab(sa, U, &cg, s->st));
                     RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
                 }
+                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
                 RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
+                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
                 RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
             }
             if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
             else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
+            RUN("cg_beta", launch_cg_finish(cg, 1, nvec, s->st));
             s->matvecs += nvec;
             CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
             CK(cudaStreamSynchronize(s->st));
@@ -952,8 +963,8 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;
-    CK(s->iterbuf.ensure(4 * sizeof(int)));
-    CK(cudaMemset(s->iterbuf.p, 0, 4 * sizeof(int)));
+    CK(s->iterbuf.ensure(8 * sizeof(int)));
+    CK(cudaMemset(s->iterbuf.p, 0, 8 * sizeof(int)));
     s->d_iter = s->iterbuf.as<int>();
     if (s->fused_ok) {
         const size_t per = cg_partials_per_vec(s->args);
@@ -998,38 +1009,52 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
         set_error("mem must be BNF_MEM_HOST or BNF_MEM_DEVICE");
         return BNF_EINVAL;
     }
+    // 1/eps, plus a compressed copy for the hot passes: uint8 index + LUT when the
+    // field has <= 256 distinct values (exact: the LUT holds the same doubles).
+    // One pass; runs of equal values (material regions) skip the table search.
+    std::vector<double> vals;
+    vals.reserve(256);
+    std::vector<unsigned char> idx(n3);
+    bool small = std::getenv("BNF_NO_EPS_LUT") == nullptr;
+    double last = -1.0;
+    int lastk = 0;
     for (long long t = 0; t < n3; ++t) {
         if (!(h[t] > 0.0) || !std::isfinite(h[t])) {
             set_error("eps must be finite and > 0");
             return BNF_EINVAL;
         }
-        h[t] = 1.0 / h[t];
+        const double inv = 1.0 / h[t];
+        h[t] = inv;
+        if (!small) continue;
+        if (inv != last) {
+            int k = -1;
+            for (int q = 0; q < (int)vals.size(); ++q)
+                if (vals[q] == inv) {
+                    k = q;
+                    break;
+                }
+            if (k < 0) {
+                if (vals.size() == 256) {
+                    small = false;
+                    continue;
+                }
+                k = (int)vals.size();
+                vals.push_back(inv);
+            }
+            last = inv;
+            lastk = k;
+        }
+        idx[t] = (unsigned char)lastk;
     }
     CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), n3 * sizeof(double), cudaMemcpyHostToDevice, s->st));
-    // Compressed copy for the hot x pass: uint8 index + LUT when <= 256 distinct values
-    // (exact: the LUT holds the same doubles).
-    std::map<double, int> lut;
-    bool small = true;
-    for (long long t = 0; t < n3 && small; ++t) {
-        if (lut.find(h[t]) == lut.end()) {
-            if (lut.size() >= 256) small = false;
-            else lut.emplace(h[t], 0);
-        }
-    }
     s->args.eps_idx = nullptr;
     s->args.eps_lut = nullptr;
-    if (small && std::getenv("BNF_NO_EPS_LUT") == nullptr) {
-        std::vector<double> vals;
-        for (auto& kv : lut) {
-            kv.second = (int)vals.size();
-            vals.push_back(kv.first);
-        }
-        std::vector<unsigned char> idx(n3);
-        for (long long t = 0; t < n3; ++t) idx[t] = (unsigned char)lut[h[t]];
+    if (small) {
         CK(s->eps_idx.ensure(n3));
         CK(s->eps_lut.ensure(256 * sizeof(double)));
+        vals.resize(256, 0.0);
         CK(cudaMemcpyAsync(s->eps_idx.p, idx.data(), n3, cudaMemcpyHostToDevice, s->st));
-        CK(cudaMemcpyAsync(s->eps_lut.p, vals.data(), vals.size() * sizeof(double), cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemcpyAsync(s->eps_lut.p, vals.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, s->st));
         s->args.eps_idx = s->eps_idx.as<unsigned char>();
         s->args.eps_lut = s->eps_lut.as<double>();
     }

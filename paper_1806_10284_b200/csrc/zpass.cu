@@ -277,7 +277,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2
         // per-CTA partial of (r, r); the last CTA of the launch forms beta
         const int nb = gridDim.x * gridDim.y;
         cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, red);
-        if (cg_last_block(cg.counter + 1 + kCgGroups, nb * gridDim.z, red)) cg_finish_beta(cg, nb, gridDim.z, red);
+        if (cg.ext) {
+            if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb;
+        } else if (cg_last_block(cg.counter + 1 + kCgGroups, nb * gridDim.z, red)) {
+            cg_finish_beta(cg, nb, gridDim.z, red);
+        }
     }
 }
 
