@@ -87,8 +87,20 @@ __device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2
     return is_last != 0;
 }
 __device__ double block_sum_fixed(const double* part, int nb, double2* scratch) {
+    // L2-coherent loads (written by other CTAs, possibly in this launch), four in
+    // flight per thread; per-thread order is fixed, so the sum is deterministic
     double acc = 0.0;
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) acc += ((volatile const double*)part)[t];
+    int t = threadIdx.x;
+    const int st = blockDim.x;
+    for (; t + 3 * st < nb; t += 4 * st) {
+        const double a0 = __ldcg(part + t), a1 = __ldcg(part + t + st);
+        const double a2 = __ldcg(part + t + 2 * st), a3 = __ldcg(part + t + 3 * st);
+        acc += a0;
+        acc += a1;
+        acc += a2;
+        acc += a3;
+    }
+    for (; t < nb; t += st) acc += __ldcg(part + t);
     __syncthreads();
     const double2 s = block_sum(make_double2(acc, 0.0), scratch);
     __shared__ double res;

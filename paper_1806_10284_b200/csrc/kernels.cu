@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restri
             double2 sum[Q];
 #pragma unroll
             for (int c = 0; c < Q; ++c) sum[c] = make_double2(0, 0);
-#pragma unroll 4
+#pragma unroll   // all 16 loads of the column slice in flight (memory-level parallelism)
             for (int r = lane; r < GT_SLICE; r += 32) {
                 const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
 #pragma unroll

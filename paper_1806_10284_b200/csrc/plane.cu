@@ -465,6 +465,8 @@ bool plane_supported(const OpArgs& a) {
 
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     if (a.plane_l2) {   // one CTA per plane, strips exchanged through L2
+        if (a.plane_cw == 64 && a.mp.n1 == 128) return launch_plane_l2_t<16, 8, 2>(a, U, nslab, cg, st);
+        if (a.plane_cw == 16 && a.mp.n1 == 128) return launch_plane_l2_t<16, 8, 8>(a, U, nslab, cg, st);
         switch (a.mp.n1) {
             case 64: return launch_plane_l2_t<8, 8, 2>(a, U, nslab, cg, st);
             case 96: return launch_plane_l2_t<24, 4, 3>(a, U, nslab, cg, st);

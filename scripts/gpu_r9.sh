@@ -1,0 +1,8 @@
+set -x
+python paper_1806_10284_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
+timeout 900 python -m pytest tests -m gpu -x -q -k "deter or graph or config1 or full_size_eigenvalues or warm" > gpurun_out/pytest_r9.log 2>&1; echo pytest rc=$?
+tail -1 gpurun_out/pytest_r9.log
+timeout 900 python bench.py --no-cpu --no-e2e > gpurun_out/bench_r9.log 2>&1; echo bench rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_r9.log').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['kpoints_per_s'], d['middle'], d['roofline']['kernel'], d['roofline']['frac']); print({k:v for k,v in d['kernel_ms'].items() if v>1})"
