@@ -1122,13 +1122,6 @@ cudaError_t fast_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaS
     switch (a.mp.n2) {
 #define BNF_CASE(NN, A, B)                                                                                    \
     case NN: {                                                                                                \
-        if (a.yw == 32 && NN >= 32 && A * B * 32 * 16 <= 160 * 1024) {                                       \
-            constexpr int W = 32;                                                                             \
-            dim3 g((a.mp.n1 + W - 1) / W, a.mp.n3, nvec > 0 ? 3 * nvec : 1);                                  \
-            const size_t sm = (size_t)fast::XchW<A, B, W>::size * sizeof(double2);                           \
-            return adjoint ? launch_k(k_ypass_fast<A, B, W, 1>, g, W * B, sm, st, U, a)                       \
-                           : launch_k(k_ypass_fast<A, B, W, 0>, g, W * B, sm, st, U, a);                      \
-        }                                                                                                     \
         constexpr int W = yW();                                                                               \
         dim3 g((a.mp.n1 + W - 1) / W, a.mp.n3, nvec > 0 ? 3 * nvec : 1);                                      \
         const size_t sm = (size_t)fast::XchW<A, B, W>::size * sizeof(double2);                               \
@@ -1363,11 +1356,5 @@ size_t cg_partials_per_vec(const OpArgs& a) {
 }
 
 
-cudaError_t launch_ypass_slab(const OpArgs& a, double2* U, int adjoint, cudaStream_t st) {
-    return fast_ypass(a, U, 0, adjoint, st);
-}
-cudaError_t launch_xpass_slab(const OpArgs& a, double2* U, const CGFuse* cg, cudaStream_t st) {
-    return fast_xpass(a, U, 0, st, cg);
-}
 
 }  // namespace bnf

@@ -54,13 +54,8 @@ struct OpArgs {
     int comp0;               // first component slab (vector*3 + l) of a split y/x launch
     int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
-    int plane_cw;            // plane pass: columns per CTA (32 default, 16 = twice the cluster size)
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
-    int yw;                     // y pass columns per CTA (16 default, 32)
-    int zunroll;                // z passes: elements per thread processed together in the mode loops (1, 2)
     int plane_l2;               // plane pass: one CTA per plane, strips exchanged through L2 (1) or cluster/DSMEM (0)
-    int plane_persist;          // plane pass: persistent clusters (1) or one cluster per plane (0)
-    long long plane_stagger;    // plane pass: start delay (cycles) of the second half of the clusters
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -92,9 +87,6 @@ struct CGFuse {
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
 cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st);
 cudaError_t launch_ypass(const OpArgs& a, double2* U, int nvec, int adjoint, cudaStream_t st);
-// one component slab (vector*3 + l = a.comp0) of the y / x passes
-cudaError_t launch_ypass_slab(const OpArgs& a, double2* U, int adjoint, cudaStream_t st);
-cudaError_t launch_xpass_slab(const OpArgs& a, double2* U, const CGFuse* cg, cudaStream_t st);
 cudaError_t launch_xpass(const OpArgs& a, double2* U, int nvec, cudaStream_t st);
 cudaError_t launch_zadj(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, cudaStream_t st);
 cudaError_t launch_xfwd_recover(const OpArgs& a, double2* U, int nvec, const double* eps_inv, double scale0,

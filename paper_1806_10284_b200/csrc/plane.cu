@@ -116,18 +116,10 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     if (epf)
         for (int q = threadIdx.x; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
     if (CG && tid < 8) acc_s[tid] = 0.0;
-    // Persistent clusters loop over the planes (component slab, z-plane).  The
-    // second half of the clusters starts half a plane late so that the two
-    // CTAs sharing an SM stay out of phase (one in its FFT phases while the
-    // other streams or exchanges).
+    // clusters loop over the planes (component slab, z-plane); the launch uses one
+    // cluster per plane (a persistent grid measured slower on B200)
     const int ncl = gridDim.x / P, cid = blockIdx.x / P;
     const int total = p.n3 * nslab;
-    if (a.plane_stagger > 0 && cid >= ncl / 2) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < a.plane_stagger) {
-        }
-        t_last = clock64();
-    }
     for (int pl = cid; pl < total; pl += ncl) {
     const int c = pl % p.n3;
     const int vl = pl / p.n3 + a.comp0;
@@ -141,21 +133,6 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
 
-    // L2 prefetch of this CTA's share of the next plane (rows of CW elements,
-    // and its eps rows) so that the next iteration's loads hit L2, not DRAM
-    if (a.plane_persist && tid < 32 && pl + ncl < total) {
-        const int c2 = (pl + ncl) % p.n3, vl2 = (pl + ncl) / p.n3 + a.comp0;
-        const double2* nxt = U + (size_t)vl2 * p.n + (size_t)c2 * N * N + (size_t)r * CW;
-        for (int j = tid; j < N; j += 32) {
-            const unsigned long long ga = (unsigned long long)(nxt + (size_t)j * N);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(ga), "r"((unsigned)(CW * 16)) : "memory");
-        }
-        if (epf && tid == 0) {
-            const unsigned char* e2 = a.eps_idx + (size_t)(vl2 % 3) * p.n + (size_t)N * ((size_t)r * CW + (size_t)N * c2);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((unsigned long long)e2),
-                         "r"((unsigned)(CW * N)) : "memory");
-        }
-    }
     // ---------------- phase Y: columns i = r*CW + w, FFT over j ----------------
     const int w = tid % CW, t = tid / CW;
     const int i = (int)r * CW + w;
@@ -425,21 +402,7 @@ cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse*
             e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             if (e != cudaSuccess) return e;
         }
-        // persistent: as many clusters as can be co-resident (cached per kernel)
-        static int ncl_max = 0;
-        if (ncl_max == 0) {
-            cfg.gridDim = dim3((unsigned)(P * total), 1, 1);
-            e = cudaOccupancyMaxActiveClusters(&ncl_max, kern, &cfg);
-            if (e != cudaSuccess || ncl_max < 1) {
-                int dev = 0, nsm = 148;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                ncl_max = std::max(1, nsm / P);
-                (void)cudaGetLastError();
-            }
-        }
-        const int ncl = a.plane_persist ? std::min(total, ncl_max) : total;
-        cfg.gridDim = dim3((unsigned)(P * ncl), 1, 1);
+        cfg.gridDim = dim3((unsigned)(P * total), 1, 1);
         return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg, nslab);
     };
     if (cg) return run(k_plane<N1, N2, P, 1>, *cg);
@@ -465,24 +428,12 @@ bool plane_supported(const OpArgs& a) {
 
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     if (a.plane_l2) {   // one CTA per plane, strips exchanged through L2
-        if (a.plane_cw == 64 && a.mp.n1 == 128) return launch_plane_l2_t<16, 8, 2>(a, U, nslab, cg, st);
-        if (a.plane_cw == 16 && a.mp.n1 == 128) return launch_plane_l2_t<16, 8, 8>(a, U, nslab, cg, st);
         switch (a.mp.n1) {
             case 64: return launch_plane_l2_t<8, 8, 2>(a, U, nslab, cg, st);
             case 96: return launch_plane_l2_t<24, 4, 3>(a, U, nslab, cg, st);
             case 128: return launch_plane_l2_t<16, 8, 4>(a, U, nslab, cg, st);
             case 192: return launch_plane_l2_t<24, 8, 6>(a, U, nslab, cg, st);
             case 256: return launch_plane_l2_t<16, 16, 8>(a, U, nslab, cg, st);
-            default: break;
-        }
-    }
-    if (a.plane_cw == 64 && a.mp.n1 == 128) return launch_plane_t<16, 8, 2>(a, U, nslab, cg, st);
-    if (a.plane_cw == 16) {   // 16 columns per CTA: smaller CTAs, twice the cluster size
-        switch (a.mp.n1) {
-            case 64: return launch_plane_t<8, 8, 4>(a, U, nslab, cg, st);
-            case 96: return launch_plane_t<24, 4, 6>(a, U, nslab, cg, st);
-            case 128: return launch_plane_t<16, 8, 8>(a, U, nslab, cg, st);
-            case 256: return launch_plane_t<16, 16, 16>(a, U, nslab, cg, st);
             default: break;
         }
     }

@@ -185,7 +185,6 @@ struct bnf_solver {
     DevBuf cgfuse_buf;
     CGFuse cgf{};
     bool fused_ok = false;
-    bool l2_slabs = false;
     bool use_plane = false;   // fused y/x/y plane pass (plane.cu)
     bool plane_ok = false;    // plane pass available for this grid
     bool plane_tuned = false; // autotune_plane done
@@ -288,15 +287,6 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
         RUN(s->args.plane_l2 ? "plane_l2" : "plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
-    } else if (s->l2_slabs) {
-        // y -> x -> y per component slab: the slab stays resident in L2 between the passes
-        OpArgs sa = s->args;
-        for (int vl = 0; vl < 3 * nvec; ++vl) {
-            sa.comp0 = vl;
-            RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
-            RUN("xpass", launch_xpass_slab(sa, U, nullptr, s->st));
-            RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
-        }
     } else {
         RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
@@ -432,16 +422,6 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     if (s->use_plane) {
         BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
         BNF_K(launch_cg_finish(cg, 0, nvec, st));
-    } else if (s->l2_slabs) {
-        OpArgs sa = s->args;
-        sa.nvec_all = nvec;
-        for (int vl = 0; vl < 3 * nvec; ++vl) {
-            sa.comp0 = vl;
-            BNF_K(launch_ypass_slab(sa, U, 0, st));
-            BNF_K(launch_xpass_slab(sa, U, &cg, st));
-            BNF_K(launch_ypass_slab(sa, U, 1, st));
-        }
-        BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
@@ -561,16 +541,6 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
-                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
-            } else if (s->l2_slabs) {
-                OpArgs sa = s->args;
-                sa.nvec_all = nvec;
-                for (int vl = 0; vl < 3 * nvec; ++vl) {
-                    sa.comp0 = vl;
-                    RUN("yfwd", launch_ypass_slab(sa, U, 0, s->st));
-                    RUN("xpass_cg", launch_xpass_slab(sa, U, &cg, s->st));
-                    RUN("yadj", launch_ypass_slab(sa, U, 1, s->st));
-                }
                 RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
@@ -942,7 +912,6 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     CK(cudaMallocHost((void**)&s->h_flags, 64 * sizeof(int)));
     s->fused_ok = fast_all(s->args) && std::getenv("BNF_NO_FUSED_CG") == nullptr;
-    s->l2_slabs = s->fused_ok && std::getenv("BNF_L2_SLABS") != nullptr;
     s->plane_ok = plane_supported(s->args);
     s->use_plane = s->plane_ok && std::getenv("BNF_NO_PLANE") == nullptr;
     {
@@ -954,12 +923,6 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
-    if (const char* cw = std::getenv("BNF_PLANE_CW")) s->args.plane_cw = std::atoi(cw);
-    s->args.plane_persist = std::getenv("BNF_PLANE_PERSIST") ? 1 : 0;
-    s->args.plane_stagger = 0;
-    s->args.yw = std::getenv("BNF_YW") ? std::atoi(std::getenv("BNF_YW")) : 16;
-    s->args.zunroll = std::getenv("BNF_Z_UNROLL") ? std::atoi(std::getenv("BNF_Z_UNROLL")) : 1;
-    if (const char* sg = std::getenv("BNF_PLANE_STAGGER")) s->args.plane_stagger = std::atoll(sg);
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

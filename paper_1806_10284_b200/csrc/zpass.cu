@@ -77,8 +77,8 @@ struct ColS {   // per-column constants shared through smem
 // CTAs per SM overlap one tile's loads with the other's FP64 work.  The
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
-template <int N1, int N2, int W, int MODE, int UNR>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2)
+template <int N1, int N2, int W, int MODE>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2
         xn2 = xcol[n + kstride * (tid / W)];
     }
     // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
-#pragma unroll(UNR)
+#pragma unroll 1
     for (int e = tid; e < TE; e += NT) {
         const int k = e / W;
         double2 u1 = sm[e], u2 = sm[TE + e];
@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2
 
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
-template <int N1, int N2, int W, int MODE, int UNR>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2)
+template <int N1, int N2, int W, int MODE>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, UNR == 1 ? BNF_Z_MINB : 2
     __syncthreads();
     // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
     double rr = 0.0;
-#pragma unroll(UNR)
+#pragma unroll 1
     for (int e = tid; e < TE; e += NT) {
         const int k = e / W;
         const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
@@ -328,27 +328,13 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_fwd(mode);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
-    if (a.zunroll == 2) {
-        if (mode) {
-            auto kern = k_zfwd2<N1, N2, W, 1, 2>;
-            cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            kern<<<g, L::C::NT, smem, st>>>(Y, U, a, 1, P, X, *cg);
-        } else {
-            auto kern = k_zfwd2<N1, N2, W, 0, 2>;
-            cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            kern<<<g, L::C::NT, smem, st>>>(Y, U, a, op, nullptr, nullptr, CGFuse{});
-        }
-        return cudaGetLastError();
-    }
     if (mode) {
-        auto kern = k_zfwd2<N1, N2, W, 1, 1>;
+        auto kern = k_zfwd2<N1, N2, W, 1>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(Y, U, a, 1, P, X, *cg);
     } else {
-        auto kern = k_zfwd2<N1, N2, W, 0, 1>;
+        auto kern = k_zfwd2<N1, N2, W, 0>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(Y, U, a, op, nullptr, nullptr, CGFuse{});
@@ -363,27 +349,13 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_adj(mode);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
-    if (a.zunroll == 2) {
-        if (mode) {
-            auto kern = k_zadj2<N1, N2, W, 1, 2>;
-            cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, 1, *cg);
-        } else {
-            auto kern = k_zadj2<N1, N2, W, 0, 2>;
-            cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, op, CGFuse{});
-        }
-        return cudaGetLastError();
-    }
     if (mode) {
-        auto kern = k_zadj2<N1, N2, W, 1, 1>;
+        auto kern = k_zadj2<N1, N2, W, 1>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, 1, *cg);
     } else {
-        auto kern = k_zadj2<N1, N2, W, 0, 1>;
+        auto kern = k_zadj2<N1, N2, W, 0>;
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, op, CGFuse{});
