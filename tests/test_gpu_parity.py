@@ -368,3 +368,50 @@ def test_plane_l2_cg_solve(bnf, monkeypatch):
     L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape)
     lam, _ = S.solve(tuple(g["kappa"]), len(g["lambda"]))
     np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+
+
+def test_abi_error_paths(bnf):
+    """Error behaviour stated in include/bnf.h: call order (ESTATE), invalid
+    eps (EINVAL), nev beyond the NFSEP dimension (EINVAL), bad op code."""
+    L = bnf.Lattice(configs.sc_vectors(), (4, 4, 4))
+    S = bnf.Solver(L)
+    y = torch.zeros(2 * 64, dtype=torch.complex128, device="cuda")
+    o = torch.empty_like(y)
+    with pytest.raises(bnf.BnfError) as e:
+        S.solve((0.1, 0.2, 0.3), 2)
+    assert e.value.code == bnf.ESTATE
+    with pytest.raises(bnf.BnfError) as e:
+        S.set_epsilon(np.full(3 * 64, -1.0))
+    assert e.value.code == bnf.EINVAL
+    with pytest.raises(bnf.BnfError) as e:
+        S.set_epsilon(np.full(3 * 64, np.inf))
+    assert e.value.code == bnf.EINVAL
+    S.set_epsilon(np.full(3 * 64, 2.0))
+    with pytest.raises(bnf.BnfError) as e:
+        S.apply_Ar(y, o, 1)
+    assert e.value.code == bnf.ESTATE
+    S.set_kappa((0.1, 0.2, 0.3))
+    with pytest.raises(bnf.BnfError) as e:
+        S.apply_Ar(y, o, 1, op=7)
+    assert e.value.code == bnf.EINVAL
+    with pytest.raises(bnf.BnfError) as e:
+        S.solve((0.1, 0.2, 0.3), 2 * 64 + 1)
+    assert e.value.code == bnf.EINVAL
+
+
+def test_device_epsilon_and_tiny_grid(bnf):
+    """eps passed as a device array equals the host path; a 2x2x2 grid (the
+    smallest with a full curl) solves to the dense oracle."""
+    a = configs.sc_vectors()
+    n = (2, 2, 2)
+    O = olat.snap(a, n)
+    eps = E.sample("random:7", n, O.a, O.delta, O.a_canon)
+    kap = (0.23, -0.11, 0.37)
+    dense = np.linalg.eigvalsh(spectral.Ar_dense(O, kap, eps))[:4]
+    L = bnf.Lattice(a, n)
+    for dev in (False, True):
+        S = bnf.Solver(L)
+        st = E.stacked(eps)
+        S.set_epsilon(torch.from_numpy(st).cuda() if dev else st)
+        lam, _ = S.solve(kap, 4)
+        np.testing.assert_allclose(lam, dense, rtol=1e-10)
