@@ -55,6 +55,7 @@ struct OpArgs {
     int nvec_all;            // vectors in the whole CG batch (split launches), 0 = grid
     const double2* hroot_z;  // e^{i pi k / n3}, k < n3 (half-angle table for lambda3 along k)
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
+    int plane_hint;             // L2 plane: evict-last / evict-first store hints (1)
     int plane_l2;               // plane pass: one CTA per plane, strips exchanged through L2 (1) or cluster/DSMEM (0)
 };
 

@@ -45,6 +45,24 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
+// Stores of the plane's intermediate strips (read back by this CTA's next
+// phase) carry an L2 evict-last policy so that they are less likely to be
+// written back to DRAM before they are overwritten; the final strips evict first.
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_hint(double2* ptr, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
 template <int P>
 struct Cluster {
     __device__ static unsigned rank() { return P == 1 ? 0u : cgx::this_cluster().block_rank(); }
@@ -289,6 +307,8 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const unsigned n12 = (unsigned)p.n12;
     const unsigned long long s3 = (unsigned long long)p.n3;
     double2 v[N1];
+    const unsigned long long pol_keep = a.plane_hint ? l2_policy_last() : 0ull;
+    const unsigned long long pol_out = a.plane_hint ? l2_policy_first() : 0ull;
     // ---------------- phase Y: column strips ----------------
     for (int r = 0; r < P; ++r) {
         const int i = r * CW + w;
@@ -303,7 +323,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+            for (int k2 = 0; k2 < N2; ++k2) {
+                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_keep);
+                else *dst = v[u * N2 + k2];
+            }
     }
     if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();   // the strips written above are read by other threads below (block scope)
@@ -331,7 +355,10 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             }
         fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
 #pragma unroll
-        for (int m = 0; m < N1; ++m) row[N2 * m + tx] = v[m];
+        for (int m = 0; m < N1; ++m) {
+            if (a.plane_hint) st_hint(row + N2 * m + tx, v[m], pol_keep);
+            else row[N2 * m + tx] = v[m];
+        }
     }
     __syncthreads();
     // ---------------- phase Y*: column strips ----------------
@@ -347,7 +374,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+            for (int k2 = 0; k2 < N2; ++k2) {
+                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_out);
+                else *dst = v[u * N2 + k2];
+            }
     }
     if (CG) {
         // this plane's (p, M p) partial; the last CTA of the launch forms alpha

@@ -923,6 +923,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
+    s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;
@@ -1252,18 +1253,19 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         TRY(gemm_nn_host(s, AZ, want, Zs, want, tmp, 1.0, 0.0));
         RUN("copy", launch_copy(AZ, tmp, N * want, s->st));
         for (int c = 0; c < want; ++c) lam[c] = w[c];
-        // residuals ||A_r y - lambda y|| (y unit): AZ_c - lambda_c Y_c
-        std::vector<cd> G1, G2, G3;
+        // residuals ||A_r y - lambda y|| / ||y||, formed explicitly (R = AZ - Y diag(lambda))
+        // rather than from Gram entries (whose cancellation would cap the resolution at
+        // ~sqrt(eps) lambda)
+        std::vector<cd> Dl((size_t)nev * nev, 0.0);
+        for (int c = 0; c < nev; ++c) Dl[(size_t)c * nev + c] = -lam[c];
+        RUN("copy", launch_copy(tmp, AZ, N * nev, s->st));
+        TRY(gemm_nn_host(s, Y, nev, Dl, nev, tmp, 1.0, 1.0));
         maxr_ar = 0.0;
         for (int c = 0; c < nev; ++c) {
-            std::vector<cd> ay, yy, aa;
-            TRY(gram_host(s, AZ + (size_t)c * N, 1, AZ + (size_t)c * N, 1, aa));
-            TRY(gram_host(s, Y + (size_t)c * N, 1, AZ + (size_t)c * N, 1, ay));
+            std::vector<cd> rr, yy;
+            TRY(gram_host(s, tmp + (size_t)c * N, 1, tmp + (size_t)c * N, 1, rr));
             TRY(gram_host(s, Y + (size_t)c * N, 1, Y + (size_t)c * N, 1, yy));
-            const double l = lam[c];
-            const double r2 = aa[0].real() - 2.0 * l * ay[0].real() + l * l * yy[0].real();
-            const double r = std::sqrt(std::fabs(r2)) / std::sqrt(yy[0].real());
-            maxr_ar = std::max(maxr_ar, r);
+            maxr_ar = std::max(maxr_ar, std::sqrt(std::fabs(rr[0].real()) / yy[0].real()));
         }
     }
     s->lam.assign(lam.begin(), lam.begin() + nev);
