@@ -30,9 +30,12 @@ def _deps():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the sources that changed (in parallel) and link libbnf.so."""
+    from concurrent.futures import ThreadPoolExecutor
+
     os.makedirs(OBJ, exist_ok=True)
     hdr_t = _deps()
-    objs = []
+    objs, jobs = [], []
     changed = force or not os.path.exists(LIB)
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -40,12 +43,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_t):
             cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
-            if src.endswith(".cu"):
-                cmd += ["-Xptxas", "-v"] if verbose else []
+            if src.endswith(".cu") and verbose:
+                cmd += ["-Xptxas", "-v"]
+            jobs.append(cmd)
+    if jobs:
+        changed = True
+
+        def run(cmd):
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-            changed = True
+
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(run, c) for c in jobs]:
+                f.result()
     if changed:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
         if verbose:
