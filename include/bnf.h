@@ -119,6 +119,8 @@ typedef struct {
     int profile;                /* 1: time every kernel with CUDA events (bnf_kernel_times) */
     int warm;                   /* 1: start each solve from the previous solve's Ritz vectors
                                    (neighbouring k on a path; DESIGN R17); 0: seeded random block */
+    int reorth_once_ok;         /* 1: skip the second Gram-Schmidt pass when the first kept every
+                                   column's norm above 1/sqrt(2) (DGKS test; DESIGN R18); 0: always twice */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);

@@ -43,7 +43,7 @@ class Opts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("tol_outer", C.c_double),
                 ("tol_inner", C.c_double), ("max_outer", C.c_int), ("max_inner", C.c_int),
                 ("block", C.c_int), ("guard", C.c_int), ("seed", C.c_ulonglong), ("refine", C.c_int),
-                ("profile", C.c_int), ("warm", C.c_int)]
+                ("profile", C.c_int), ("warm", C.c_int), ("reorth_once_ok", C.c_int)]
 
 
 class Stats(C.Structure):

@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
-        if (cg.ext) {
+        if (cg.ext_a) {
             if (lin == 0 && threadIdx.x == 0) *cg.nb_x = nb;
         } else if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) {
             cg_finish_alpha(cg, nb, nvec_all, sm);

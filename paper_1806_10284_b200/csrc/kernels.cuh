@@ -78,7 +78,8 @@ struct CGFuse {
     int* active;
     int* nb_x;                         // partial counts per vector written by the producing passes
     int* nb_z;                         //   (ext mode: reduced by k_cg_finish after the pass)
-    int ext;                           // 1: scalars formed by k_cg_finish (no in-kernel last-CTA election)
+    int ext;                           // 1: beta formed by k_cg_finish after zadj (no in-kernel election)
+    int ext_a;                         // 1: alpha formed by k_cg_finish after the (p, M p) pass
     int* iter;                         // CG iterations done (device), or null
     int max_iter;
     int use_cond;                      // 1: set the CG graph's while-condition

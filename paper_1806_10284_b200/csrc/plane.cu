@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int nb = gridDim.x;
         if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
         __syncthreads();
-        if (cgf.ext) {
+        if (cgf.ext_a) {
             if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;
         } else if (cg_last_block(cgf.counter + 0, nb, D)) {
             cg_finish_alpha(cgf, nb, nvec, D);
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (cgf.ext) {
+        if (cgf.ext_a) {
             if (lin == 0 && tid == 0) *cgf.nb_x = nb;
         } else if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D, lin)) {
             cg_finish_alpha(cgf, nb, nvec_all, D);

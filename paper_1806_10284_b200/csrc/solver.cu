@@ -210,6 +210,7 @@ struct bnf_solver {
     std::vector<double> lam;
     int nev_last = 0;
     int prev_want = 0;   // Ritz vectors of the last solve kept in Yv (warm start)
+    long long reorth_skipped = 0;   // DGKS second passes skipped (diagnostics)
     int* h_flags = nullptr;     // pinned
     double2* h_small = nullptr;  // pinned scratch for small matrices
     size_t h_small_cap = 0;
@@ -421,7 +422,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
         BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
-        BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        if (cg.ext_a) BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
@@ -519,7 +520,10 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     CGFuse cg = s->cgf;
     cg.P = P;
     cg.R = R;
-    cg.ext = 1;   // CG scalars by k_cg_finish after each reducing pass
+    cg.ext = 1;   // beta by k_cg_finish after zadj (thousands of CTAs: no per-CTA fences)
+    // alpha: the plane pass has few, long CTAs, where the in-kernel last-CTA election is
+    // cheaper than one more launch; the x pass has many short CTAs -> k_cg_finish
+    cg.ext_a = s->use_plane ? (std::getenv("BNF_CG_EXT_A") ? 1 : 0) : 1;
     cg.nb_x = s->d_iter + 4;
     cg.nb_z = s->d_iter + 5;
     int it = 0;
@@ -541,7 +545,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
-                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
+                if (cg.ext_a) RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
                 RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
@@ -793,6 +797,8 @@ void bnf_opts_default(bnf_opts* o) {
     o->seed = 0x5EEDull;
     o->refine = 1;
     o->profile = 0;
+    o->warm = 0;
+    o->reorth_once_ok = 1;
 }
 
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
@@ -1122,13 +1128,30 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     for (int step = 0; step < maxsteps; ++step) {
         double2* Vj = V + (size_t)step * b * N;
         TRY(apply_Ar_inv(s, Vj, W, b));  // W = A_r^{-1} V_j
-        // full reorthogonalisation, twice (DGKS); accumulate the projections
+        // full reorthogonalisation (classical Gram-Schmidt against all of V) with the
+        // DGKS / Kahan-Parlett "twice is enough" test: the second pass runs unless the
+        // first kept every column's norm above 1/sqrt(2) of its value (norm after the
+        // pass from Pythagoras, V orthonormal); accumulate the projections
         const int p = (step + 1) * b;
-        std::vector<cd> Hacc((size_t)p * b, 0.0), H;
+        std::vector<cd> Hacc((size_t)p * b, 0.0), H, G0;
+        TRY(gram_host(s, W, b, W, b, G0));
         for (int pass = 0; pass < 2; ++pass) {
             TRY(gram_host(s, V, p, W, b, H));
             TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
             for (size_t t = 0; t < H.size(); ++t) Hacc[t] += H[t];
+            if (pass == 0 && s->o.reorth_once_ok) {
+                bool keep = true;
+                for (int c = 0; c < b && keep; ++c) {
+                    double proj = 0.0;
+                    for (int a = 0; a < p; ++a) proj += std::norm(H[(size_t)a * b + c]);
+                    const double w0 = G0[(size_t)c * b + c].real();
+                    keep = (w0 - proj) >= 0.5 * w0;
+                }
+                if (keep) {
+                    s->reorth_skipped++;
+                    break;
+                }
+            }
         }
         std::vector<cd> A((size_t)b * b);
         for (int i = 0; i < b; ++i)
