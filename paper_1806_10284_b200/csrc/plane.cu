@@ -292,9 +292,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
     double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
-    constexpr bool EPF = (N % 16) == 0;
+    constexpr bool EPF = (N % 16) == 0 && N <= 128;   // whole-plane index prefetch fits next to D
     unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);   // [N][N] material indices
-    double* lut_s = reinterpret_cast<double*>(eps_s + N * N);
+    double* lut_s = reinterpret_cast<double*>(eps_s + (EPF ? N * N : 0));
     const bool epf = EPF && a.eps_idx != nullptr;
     if (epf) {
         for (int q = tid; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
@@ -398,7 +398,8 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 template <int N1, int N2, int P>
 cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
-    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (size_t)C::N * C::N + 256 * sizeof(double);
+    constexpr bool EPF = (C::N % 16) == 0 && C::N <= 128;
+    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (EPF ? (size_t)C::N * C::N : 0) + 256 * sizeof(double);
     const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -464,7 +465,7 @@ cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* c
             case 96: return launch_plane_l2_t<24, 4, 3>(a, U, nslab, cg, st);
             case 128: return launch_plane_l2_t<16, 8, 4>(a, U, nslab, cg, st);
             case 192: return launch_plane_l2_t<24, 8, 6>(a, U, nslab, cg, st);
-            case 256: return launch_plane_l2_t<16, 16, 8>(a, U, nslab, cg, st);
+            case 256: return launch_plane_l2_t<16, 16, 16>(a, U, nslab, cg, st);   // 16-column strips: 2 CTAs/SM
             default: break;
         }
     }

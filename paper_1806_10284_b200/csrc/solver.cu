@@ -521,9 +521,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     cg.P = P;
     cg.R = R;
     cg.ext = 1;   // beta by k_cg_finish after zadj (thousands of CTAs: no per-CTA fences)
-    // alpha: the plane pass has few, long CTAs, where the in-kernel last-CTA election is
-    // cheaper than one more launch; the x pass has many short CTAs -> k_cg_finish
-    cg.ext_a = s->use_plane ? (std::getenv("BNF_CG_EXT_A") ? 1 : 0) : 1;
+    cg.ext_a = 1;   // alpha by k_cg_finish after the (p, M p) pass (in-kernel election measured no faster)
     cg.nb_x = s->d_iter + 4;
     cg.nb_z = s->d_iter + 5;
     int it = 0;
