@@ -121,6 +121,10 @@ typedef struct {
                                    (neighbouring k on a path; DESIGN R17); 0: seeded random block */
     int reorth_once_ok;         /* 1: skip the second Gram-Schmidt pass when the first kept every
                                    column's norm above 1/sqrt(2) (DGKS test; DESIGN R18); 0: always twice */
+    double res_tol;             /* 5e-9: with refine >= 1, repeat a step of subspace inverse iteration +
+                                   Rayleigh-Ritz while max ||A_r y - lambda y|| / ||y|| > res_tol
+                                   (north-star eigenvector bar 1e-8; DESIGN R19) */
+    int max_polish;             /* at most this many such extra steps (3) */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);
@@ -134,6 +138,7 @@ typedef struct {
     double max_ritz_residual;   /* max_i |beta s_i| / |theta_i| at exit (A_r^{-1} Ritz pairs) */
     double max_residual;        /* max_i ||A_r y_i - lambda_i y_i|| / ||y_i|| of the returned pairs */
     double seconds;             /* wall time of the call */
+    int polish_steps;           /* extra inverse-iteration + Rayleigh-Ritz steps taken for res_tol */
 } bnf_stats;
 
 /* Create a solver for a lattice on opts->device.  Allocates device memory

@@ -43,13 +43,15 @@ class Opts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("tol_outer", C.c_double),
                 ("tol_inner", C.c_double), ("max_outer", C.c_int), ("max_inner", C.c_int),
                 ("block", C.c_int), ("guard", C.c_int), ("seed", C.c_ulonglong), ("refine", C.c_int),
-                ("profile", C.c_int), ("warm", C.c_int), ("reorth_once_ok", C.c_int)]
+                ("profile", C.c_int), ("warm", C.c_int), ("reorth_once_ok", C.c_int),
+                ("res_tol", C.c_double), ("max_polish", C.c_int)]
 
 
 class Stats(C.Structure):
     _fields_ = [("outer_steps", C.c_int), ("converged", C.c_int), ("inner_iters", C.c_longlong),
                 ("matvecs", C.c_longlong), ("kernel_launches", C.c_longlong),
-                ("max_ritz_residual", C.c_double), ("max_residual", C.c_double), ("seconds", C.c_double)]
+                ("max_ritz_residual", C.c_double), ("max_residual", C.c_double), ("seconds", C.c_double),
+                ("polish_steps", C.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -797,6 +797,8 @@ void bnf_opts_default(bnf_opts* o) {
     o->profile = 0;
     o->warm = 0;
     o->reorth_once_ok = 1;
+    o->res_tol = 5e-9;
+    o->max_polish = 3;
 }
 
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
@@ -1238,10 +1240,12 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     std::vector<double> lam(want);
     for (int c = 0; c < want; ++c) lam[c] = 1.0 / theta[c];
     double maxr_ar = -1.0;
-    if (s->o.refine >= 1) {
-        // Rayleigh-Ritz of A_r on span(Y) (DESIGN R15); optional one step of
-        // subspace (inverse) iteration first.
-        if (s->o.refine >= 2) {
+    int polish = 0;
+    if (s->o.refine >= 1) for (int pass = 0;; ++pass) {
+        // Rayleigh-Ritz of A_r on span(Y) (DESIGN R15); a step of subspace
+        // (inverse) iteration first when refine >= 2, and again while the
+        // explicit residual of a returned pair exceeds res_tol (DESIGN R19).
+        if (s->o.refine >= 2 || pass > 0) {
             for (int c0 = 0; c0 < want; c0 += b) {
                 const int qc = std::min(b, want - c0);
                 TRY(apply_Ar_inv(s, Y + (size_t)c0 * N, s->cgx.as<double2>(), qc));
@@ -1288,6 +1292,8 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
             TRY(gram_host(s, Y + (size_t)c * N, 1, Y + (size_t)c * N, 1, yy));
             maxr_ar = std::max(maxr_ar, std::sqrt(std::fabs(rr[0].real()) / yy[0].real()));
         }
+        if (!(maxr_ar > s->o.res_tol) || pass >= s->o.max_polish) break;
+        ++polish;
     }
     s->lam.assign(lam.begin(), lam.begin() + nev);
     s->nev_last = nev;
@@ -1311,6 +1317,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         stats->kernel_launches = s->prof.launches - launches0 + graph_launches;
         stats->max_ritz_residual = maxres;
         stats->max_residual = maxr_ar;
+        stats->polish_steps = polish;
         stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     if (!converged) {

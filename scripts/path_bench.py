@@ -62,6 +62,8 @@ def main():
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "matvecs_per_kpoint": float(np.mean([r.stats["matvecs"] for r in recs])),
                 "max_residual": max(r.stats["max_residual"] for r in recs),
+                "residual_per_k": [float("%.3g" % r.stats["max_residual"]) for r in recs],
+                "polish_steps_per_k": [int(r.stats.get("polish_steps", 0)) for r in recs],
                 "golden_kpoints": len(dev), "max_rel_dev_vs_oracle": max(dev) if dev else None,
                 "lambda_first_k": recs[0].lam[:4], "omega_over_2pi_first_k": kpath.frequencies(recs[0].lam[:4])}
         print(json.dumps(line), flush=True)

@@ -31,7 +31,8 @@ def main():
     lat = bnf.Lattice(cfg.a_raw, cfg.n)
     S = bnf.Solver(lat)
     S.set_epsilon(eps_for(cfg, lat))
-    S.set_kappa(kappas(cfg, lat)[1])
+    ks = kappas(cfg, lat)
+    S.set_kappa(ks[min(1, len(ks) - 1)])
     n = lat.nn
     y = torch.randn(a.b * 2 * n, dtype=torch.complex128, device="cuda")
     o = torch.empty_like(y)

@@ -415,3 +415,33 @@ def test_device_epsilon_and_tiny_grid(bnf):
         S.set_epsilon(torch.from_numpy(st).cuda() if dev else st)
         lam, _ = S.solve(kap, 4)
         np.testing.assert_allclose(lam, dense, rtol=1e-10)
+
+
+def test_residual_polish(bnf):
+    """DESIGN R19: with res_tol below any attainable residual, exactly
+    max_polish extra inverse-iteration + Rayleigh-Ritz steps run; they leave
+    the eigenvalues (converged to 1e-12 already) unchanged to 1e-10 and do not
+    raise the residual above the north-star bar."""
+    cfg, n, kap = _cfg_case(2, (16, 16, 16), 9)
+    L, O, eps, S0 = _setup(bnf, cfg.a_raw, n, cfg.shape)
+    l0, s0 = S0.solve(kap, 8)
+    _, _, _, S1 = _setup(bnf, cfg.a_raw, n, cfg.shape, res_tol=1e-300, max_polish=2)
+    l1, s1 = S1.solve(kap, 8)
+    assert s0["polish_steps"] == 0 and s1["polish_steps"] == 2
+    assert s1["matvecs"] > s0["matvecs"]
+    np.testing.assert_allclose(l1, l0, rtol=1e-10)
+    assert s1["max_residual"] <= 1e-8
+
+
+def test_path_residuals_config4(bnf):
+    """The first k-points of config 4's path at full 128^3 with warm start (the
+    bench's mode): every returned pair meets ||A_r y - lambda y|| / ||y|| <= 1e-8
+    (the second k-point needed one polish step before R19)."""
+    from paper_1806_10284_b200 import kpath
+    cfg = configs.config(4)
+    lat = bnf.Lattice(cfg.a_raw, cfg.n)
+    eps = E.stacked(E.sample(cfg.shape, cfg.n, lat.a, lat.delta, lat.a_canon))
+    kaps = [tuple(lat.kappa_from_raw(K)) for K in cfg.kappa_direct[:3]]
+    recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, kaps, cfg.nev, device=0, warm=1)
+    assert all(r.status == "ok" for r in recs)
+    assert max(r.stats["max_residual"] for r in recs) <= 1e-8
