@@ -108,37 +108,42 @@ __device__ double block_sum_fixed(const double* part, int nb, double2* scratch) 
     __syncthreads();
     return res;
 }
+// CG scalar updates of one vector from its reduced (p, M p) resp. (r, r)
+__device__ __forceinline__ void cg_alpha_update(const CGFuse& cg, int v, double pmp) {
+    cg.pmp[v] = pmp;
+    cg.alpha[v] = (cg.active[v] && pmp > 0.0) ? cg.rr[v] / pmp : 0.0;
+}
+__device__ __forceinline__ void cg_beta_update(const CGFuse& cg, int v, double rn) {
+    const int act = cg.active[v];
+    cg.beta[v] = (act && cg.rr[v] > 0.0) ? rn / cg.rr[v] : 0.0;
+    if (act) cg.rr[v] = rn;
+    cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;
+}
+// device-side loop control of the CG graph (solver.cu, cg_graph): continue while
+// any vector is active and the iteration cap is not reached (thread 0, after the
+// beta updates of every vector are visible to it)
+__device__ __forceinline__ void cg_loop_control(const CGFuse& cg, int nvec) {
+    if (cg.iter != nullptr) {
+        int any = 0;
+        for (int v = 0; v < nvec; ++v) any |= cg.active[v];
+        const int it = ++cg.iter[0];
+        cg.iter[1] += 1;
+        cg.iter[2] += nvec;
+        if (cg.use_cond) cudaGraphSetConditional(cg.cond, (any && it < cg.max_iter) ? 1u : 0u);
+    }
+}
 __device__ __noinline__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
     for (int v = 0; v < nvec; ++v) {
         const double pmp = block_sum_fixed(cg.part_x + (size_t)v * nb, nb, scratch);
-        if (threadIdx.x == 0) {
-            cg.pmp[v] = pmp;
-            cg.alpha[v] = (cg.active[v] && pmp > 0.0) ? cg.rr[v] / pmp : 0.0;
-        }
+        if (threadIdx.x == 0) cg_alpha_update(cg, v, pmp);
     }
 }
 __device__ __noinline__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
     for (int v = 0; v < nvec; ++v) {
         const double rn = block_sum_fixed(cg.part_z + (size_t)v * nb, nb, scratch);
-        if (threadIdx.x == 0) {
-            const int act = cg.active[v];
-            cg.beta[v] = (act && cg.rr[v] > 0.0) ? rn / cg.rr[v] : 0.0;
-            if (act) cg.rr[v] = rn;
-            cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;
-        }
+        if (threadIdx.x == 0) cg_beta_update(cg, v, rn);
     }
-    if (threadIdx.x == 0) {
-        // device-side loop control of the CG graph (solver.cu, cg_graph): continue
-        // while any vector is active and the iteration cap is not reached
-        if (cg.iter != nullptr) {
-            int any = 0;
-            for (int v = 0; v < nvec; ++v) any |= cg.active[v];
-            const int it = ++cg.iter[0];
-            cg.iter[1] += 1;
-            cg.iter[2] += nvec;
-            if (cg.use_cond) cudaGraphSetConditional(cg.cond, (any && it < cg.max_iter) ? 1u : 0u);
-        }
-    }
+    if (threadIdx.x == 0) cg_loop_control(cg, nvec);
 }
 
 }  // namespace

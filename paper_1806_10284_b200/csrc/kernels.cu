@@ -1042,10 +1042,46 @@ __global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restr
 // CG scalars from the per-CTA partials of the preceding pass (one CTA, fixed
 // summation order): the kernel boundary orders the partials, so the passes
 // need no fences or atomics.
+// CG scalars after a pass (which = 0: alpha from the (p, M p) partials, 1: beta
+// from the (r, r) partials + loop control).  The 32 warps are split evenly over
+// the vectors (up to 32 per round), so all vectors' partials are in flight at
+// once; every sum is taken in a fixed order (deterministic).
 __global__ void __launch_bounds__(1024) k_cg_finish(CGFuse cg, int which, int nvec) {
-    __shared__ double2 red[32];
-    if (which == 0) cg_finish_alpha(cg, *cg.nb_x, nvec, red);
-    else cg_finish_beta(cg, *cg.nb_z, nvec, red);
+    __shared__ double wsum[32];
+    const int nb = which == 0 ? *cg.nb_x : *cg.nb_z;
+    const double* part = which == 0 ? cg.part_x : cg.part_z;
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int v0 = 0; v0 < nvec; v0 += nw) {
+        const int nv = min(nvec - v0, nw), wpv = nw / nv;
+        const int vl = warp / wpv, wi = warp % wpv;
+        double acc = 0.0;
+        if (vl < nv) {
+            const double* pp = part + (size_t)(v0 + vl) * nb;
+            const int st = wpv * 32;
+            int t = wi * 32 + lane;
+            for (; t + 3 * st < nb; t += 4 * st) {
+                const double a0 = __ldcg(pp + t), a1 = __ldcg(pp + t + st);
+                const double a2 = __ldcg(pp + t + 2 * st), a3 = __ldcg(pp + t + 3 * st);
+                acc += a0;
+                acc += a1;
+                acc += a2;
+                acc += a3;
+            }
+            for (; t < nb; t += st) acc += __ldcg(pp + t);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) wsum[warp] = acc;
+        __syncthreads();
+        if ((int)threadIdx.x < nv) {
+            double sv = 0.0;
+            for (int q = 0; q < wpv; ++q) sv += wsum[threadIdx.x * wpv + q];
+            if (which == 0) cg_alpha_update(cg, v0 + threadIdx.x, sv);
+            else cg_beta_update(cg, v0 + threadIdx.x, sv);
+        }
+        __syncthreads();
+    }
+    if (which == 1 && threadIdx.x == 0) cg_loop_control(cg, nvec);
 }
 
 inline int grid_for(long long total, int threads, int cap = 148 * 16) {
