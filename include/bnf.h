@@ -105,6 +105,21 @@ void bnf_lattice_destroy(bnf_lattice* lat);
    canonical vectors.  Host-only. */
 int bnf_kvec_reduce(const bnf_lattice* lat, const double K_cart[3], double kappa[3]);
 
+/* Yee points of component comp (0, 1, 2) at which B_comp is sampled
+   (the edge midpoints x(a+1/2,b,c), x(a,b+1/2,c), x(a,b,c+1/2)
+   of the grid of the snapped lattice).  xyz: HOST, n1*n2*n3 rows
+   of 3 doubles, x fastest (row a + n1 (b + n2 c)); caller-owned.
+   frame = BNF_FRAME_SNAPPED: Cartesian coordinates ((a+h1)dx, (b+h2)dy,
+   (c+h3)dz) in the transformed frame of the corrected vectors a1..a3;
+   BNF_FRAME_ORIGINAL: the point's fractional coordinates in the snapped cell,
+   wrapped into [0, 1)^3, applied to the canonical raw vectors a_canon (the
+   original Cartesian frame; the map used to sample shapes defined there,
+   DESIGN §4).  BNF_EINVAL on a NULL pointer, comp or frame out of range.
+   Host-only. */
+#define BNF_FRAME_SNAPPED 0
+#define BNF_FRAME_ORIGINAL 1
+int bnf_yee_points(const bnf_lattice* lat, int comp, int frame, double* xyz);
+
 typedef struct {
     int device;                 /* CUDA device ordinal */
     void* stream;               /* cudaStream_t to issue work on; NULL = legacy default stream */

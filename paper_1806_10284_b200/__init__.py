@@ -65,6 +65,7 @@ _sigs = {
     "bnf_lattice_create": [C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(_P)],
     "bnf_lattice_query": [_P, C.POINTER(LatticeInfo)],
     "bnf_kvec_reduce": [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bnf_yee_points": [_P, C.c_int, C.c_int, C.POINTER(C.c_double)],
     "bnf_solver_create": [_P, C.POINTER(Opts), C.POINTER(_P)],
     "bnf_set_epsilon": [_P, _P, C.c_int],
     "bnf_set_kappa": [_P, C.POINTER(C.c_double)],
@@ -88,7 +89,9 @@ _lib.bnf_solver_destroy.restype = None
 _lib.bnf_opts_default.argtypes = [C.POINTER(Opts)]
 _lib.bnf_opts_default.restype = None
 
-EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce",
+FRAME_SNAPPED, FRAME_ORIGINAL = 0, 1
+
+EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce", "bnf_yee_points",
            "bnf_opts_default", "bnf_solver_create", "bnf_solver_destroy", "bnf_set_epsilon", "bnf_set_kappa",
            "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile", "bnf_phase_counters",
            "bnf_last_error", "bnf_version", "bnf_host_herm_eig"]
@@ -139,6 +142,13 @@ class Lattice:
         out = _D3()
         _check(_lib.bnf_kvec_reduce(self._h, _D3(*[float(x) for x in K]), out))
         return tuple(out)
+
+    def yee_points(self, comp, frame=0):
+        """(n, 3) float64 Yee points of component comp: frame 0 = snapped
+        (transformed) frame, 1 = original frame (bnf_yee_points)."""
+        out = np.empty((self.nn, 3), dtype=np.float64)
+        _check(_lib.bnf_yee_points(self._h, int(comp), int(frame), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def kappa_from_raw(self, kappa_raw):
         k = [float(kappa_raw[self.perm[l]]) for l in range(3)]

@@ -781,6 +781,47 @@ int bnf_kvec_reduce(const bnf_lattice* lat, const double K[3], double kappa[3]) 
     return BNF_OK;
 }
 
+int bnf_yee_points(const bnf_lattice* lat, int comp, int frame, double* xyz) {
+    if (!lat || !xyz) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    if (comp < 0 || comp > 2 || (frame != BNF_FRAME_SNAPPED && frame != BNF_FRAME_ORIGINAL)) {
+        set_error("bnf_yee_points: comp must be 0..2 and frame BNF_FRAME_SNAPPED or BNF_FRAME_ORIGINAL");
+        return BNF_EINVAL;
+    }
+    const Lattice& L = lat->L;
+    const int n1 = L.n[0], n2 = L.n[1], n3 = L.n[2];
+    // a (snapped, upper triangular, columns a[3*l + r]) inverse by back substitution
+    const double* A = L.a;
+    const double a11 = A[0], a12 = A[3], a13 = A[6], a22 = A[4], a23 = A[7], a33 = A[8];
+    size_t q = 0;
+    for (int c = 0; c < n3; ++c)
+        for (int b = 0; b < n2; ++b)
+            for (int a = 0; a < n1; ++a, ++q) {
+                const double x = (a + (comp == 0 ? 0.5 : 0.0)) * L.delta[0];
+                const double y = (b + (comp == 1 ? 0.5 : 0.0)) * L.delta[1];
+                const double z = (c + (comp == 2 ? 0.5 : 0.0)) * L.delta[2];
+                double* o = xyz + 3 * q;
+                if (frame == BNF_FRAME_SNAPPED) {
+                    o[0] = x;
+                    o[1] = y;
+                    o[2] = z;
+                    continue;
+                }
+                // fractional coordinates f = a^{-1} (x, y, z), wrapped into [0, 1)
+                double f3 = z / a33;
+                double f2 = (y - a23 * f3) / a22;
+                double f1 = (x - a12 * f2 - a13 * f3) / a11;
+                f1 -= std::floor(f1);
+                f2 -= std::floor(f2);
+                f3 -= std::floor(f3);
+                for (int r = 0; r < 3; ++r)
+                    o[r] = L.a_canon[r] * f1 + L.a_canon[3 + r] * f2 + L.a_canon[6 + r] * f3;
+            }
+    return BNF_OK;
+}
+
 void bnf_opts_default(bnf_opts* o) {
     if (!o) return;
     std::memset(o, 0, sizeof(*o));

@@ -57,6 +57,38 @@ def test_lattice_bit_equal_to_oracle(bnf, idx):
             np.testing.assert_allclose(L.kvec_reduce(K), olat.kvec_reduce(O, K), atol=1e-15)
 
 
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_yee_points(bnf, idx):
+    """bnf_yee_points (P:L323-332 edge midpoints): the snapped-frame points are
+    ((a+h1)dx, (b+h2)dy, (c+h3)dz) x-fastest; the original-frame points are the
+    wrapped fractional coordinates in the snapped cell applied to a_canon --
+    the map the synthetic eps sampler uses, so sampling the shapes at them
+    reproduces the sampler's eps field exactly."""
+    from synthetic import configs, eps as E
+    cfg = configs.config(idx)
+    n = cfg.n if idx < 4 else (16, 12, 10)
+    L = bnf.Lattice(cfg.a_raw, n)
+    inv = np.linalg.inv(L.a)
+    for comp in range(3):
+        xs = L.yee_points(comp, bnf.FRAME_SNAPPED)
+        np.testing.assert_array_equal(xs, E.yee_points(L.delta, n, comp))
+        f = xs @ inv.T
+        f -= np.floor(f)
+        xo = L.yee_points(comp, bnf.FRAME_ORIGINAL)
+        # same fractional coordinates modulo the lattice (a point on a cell face may wrap to
+        # either side, depending on the last bit of its coordinate), inside the canonical cell
+        g = np.linalg.solve(L.a_canon, xo.T).T
+        assert g.min() > -1e-12 and g.max() < 1 + 1e-12
+        d = g - f
+        assert np.abs(d - np.round(d)).max() <= 1e-12
+    if cfg.shape != "noise42":
+        e_s = E.sample(cfg.shape, n, L.a, L.delta, L.a_canon)[1].ravel()
+        inside = E._inside(L.yee_points(1, bnf.FRAME_ORIGINAL), cfg.shape, L.a_canon)
+        np.testing.assert_array_equal(np.where(inside, E.EPS_IN, E.EPS_OUT), e_s)
+    with pytest.raises(bnf.BnfError):
+        L.yee_points(3)
+
+
 def test_lattice_random_bit_equal(bnf):
     from oracle import lattice as olat
     from tests.test_oracle_curl import random_lattices
