@@ -320,14 +320,17 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
         const double2 wk = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3));
         fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
+        if (a.plane_hint) {
 #pragma unroll
-        for (int u = 0; u < N1 / N2; ++u)
+            for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
-                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_keep);
-                else *dst = v[u * N2 + k2];
-            }
+                for (int k2 = 0; k2 < N2; ++k2) st_hint(plane + (size_t)(t + N2 * u + N1 * k2) * N + i, v[u * N2 + k2], pol_keep);
+        } else {
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+        }
     }
     if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();   // the strips written above are read by other threads below (block scope)
@@ -340,24 +343,29 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + tx];
         fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
         const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+        // 1/(n eps) scaling (+ CG partial); the ε source is chosen once per strip, not per element
+        auto scale = [&](auto eps_at) {
 #pragma unroll
-        for (int u = 0; u < N1 / N2; ++u)
+            for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                const int aa = tx + N2 * u + N1 * k2;
-                const double e_ = epf ? lut_s[eps_s[b * N + aa]]
-                                      : (a.eps_idx ? __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa))
-                                                   : __ldg(a.eps_inv + rowofs + aa));
-                const double s_ = a.inv_n * e_;
-                const double2 x = v[u * N2 + k2];
-                if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
-                v[u * N2 + k2] = cscale(x, s_);
-            }
+                for (int k2 = 0; k2 < N2; ++k2) {
+                    const int aa = tx + N2 * u + N1 * k2;
+                    const double s_ = a.inv_n * eps_at(aa);
+                    const double2 x = v[u * N2 + k2];
+                    if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
+                    v[u * N2 + k2] = cscale(x, s_);
+                }
+        };
+        if (epf) scale([&](int aa) { return lut_s[eps_s[b * N + aa]]; });
+        else if (a.eps_idx) scale([&](int aa) { return __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa)); });
+        else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
         fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
+        if (a.plane_hint) {
 #pragma unroll
-        for (int m = 0; m < N1; ++m) {
-            if (a.plane_hint) st_hint(row + N2 * m + tx, v[m], pol_keep);
-            else row[N2 * m + tx] = v[m];
+            for (int m = 0; m < N1; ++m) st_hint(row + N2 * m + tx, v[m], pol_keep);
+        } else {
+#pragma unroll
+            for (int m = 0; m < N1; ++m) row[N2 * m + tx] = v[m];
         }
     }
     __syncthreads();
@@ -371,14 +379,17 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
         fast::twiddle_natural<N1, N2>(v, wt, wu);
         fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
+        if (a.plane_hint) {
 #pragma unroll
-        for (int u = 0; u < N1 / N2; ++u)
+            for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
-                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_out);
-                else *dst = v[u * N2 + k2];
-            }
+                for (int k2 = 0; k2 < N2; ++k2) st_hint(plane + (size_t)(t + N2 * u + N1 * k2) * N + i, v[u * N2 + k2], pol_out);
+        } else {
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+        }
     }
     if (CG) {
         // this plane's (p, M p) partial; the last CTA of the launch forms alpha
