@@ -47,66 +47,13 @@ __device__ double2 block_sum(double2 v, double2* red) {
 }
 
 // ---------------------------------------------- fused-CG reductions
-// Block partial of one double (written by thread 0), then a "last block
-// done" election; the last block reduces all partials in a fixed order
-// (deterministic) and updates the CG scalars.
+// Block partial of one double (written by thread 0); k_cg_finish (kernels.cu)
+// reduces the partials of a launch in a fixed order (deterministic) and
+// updates the CG scalars.
 __device__ void cg_block_partial(double v, double* slot, double2* scratch) {
     __syncthreads();   // scratch (shared memory) may still be in use
     const double2 s = block_sum(make_double2(v, 0.0), scratch);
     if (threadIdx.x == 0) *slot = s.x;
-}
-// "Last CTA done" election over `total` CTAs with a two-level counter
-// (kCgGroups sub-counters + one top counter, laid out [top][sub...]) so that
-// thousands of CTAs do not serialise on one L2 atomic.  The elected CTA
-// resets all counters (every CTA has arrived by then).
-constexpr int kCgGroups = 64;
-// lin: this CTA's index among the `total` (default: its linear index in the grid;
-// split launches pass their global index)
-__device__ bool cg_last_block(unsigned int* counter, unsigned int total, double2* scratch, long long lin_in = -1) {
-    __shared__ int is_last;
-    if (threadIdx.x == 0) {
-        const unsigned int lin = lin_in >= 0 ? (unsigned int)lin_in
-                                             : blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-        const unsigned int ng = total < (unsigned)kCgGroups ? total : (unsigned)kCgGroups;
-        const unsigned int g = lin % ng;
-        const unsigned int gsize = total / ng + (g < total % ng ? 1u : 0u);
-        __threadfence();
-        int last = 0;
-        if (atomicAdd(counter + 1 + g, 1u) == gsize - 1) {
-            __threadfence();
-            last = (atomicAdd(counter, 1u) == ng - 1) ? 1 : 0;
-        }
-        if (last) {
-            counter[0] = 0u;
-            for (unsigned int q = 0; q < ng; ++q) counter[1 + q] = 0u;
-        }
-        is_last = last;
-    }
-    __syncthreads();
-    if (is_last) __threadfence();
-    return is_last != 0;
-}
-__device__ double block_sum_fixed(const double* part, int nb, double2* scratch) {
-    // L2-coherent loads (written by other CTAs, possibly in this launch), four in
-    // flight per thread; per-thread order is fixed, so the sum is deterministic
-    double acc = 0.0;
-    int t = threadIdx.x;
-    const int st = blockDim.x;
-    for (; t + 3 * st < nb; t += 4 * st) {
-        const double a0 = __ldcg(part + t), a1 = __ldcg(part + t + st);
-        const double a2 = __ldcg(part + t + 2 * st), a3 = __ldcg(part + t + 3 * st);
-        acc += a0;
-        acc += a1;
-        acc += a2;
-        acc += a3;
-    }
-    for (; t < nb; t += st) acc += __ldcg(part + t);
-    __syncthreads();
-    const double2 s = block_sum(make_double2(acc, 0.0), scratch);
-    __shared__ double res;
-    if (threadIdx.x == 0) res = s.x;
-    __syncthreads();
-    return res;
 }
 // CG scalar updates of one vector from its reduced (p, M p) resp. (r, r)
 __device__ __forceinline__ void cg_alpha_update(const CGFuse& cg, int v, double pmp) {
@@ -132,19 +79,5 @@ __device__ __forceinline__ void cg_loop_control(const CGFuse& cg, int nvec) {
         if (cg.use_cond) cudaGraphSetConditional(cg.cond, (any && it < cg.max_iter) ? 1u : 0u);
     }
 }
-__device__ __noinline__ void cg_finish_alpha(const CGFuse& cg, int nb, int nvec, double2* scratch) {
-    for (int v = 0; v < nvec; ++v) {
-        const double pmp = block_sum_fixed(cg.part_x + (size_t)v * nb, nb, scratch);
-        if (threadIdx.x == 0) cg_alpha_update(cg, v, pmp);
-    }
-}
-__device__ __noinline__ void cg_finish_beta(const CGFuse& cg, int nb, int nvec, double2* scratch) {
-    for (int v = 0; v < nvec; ++v) {
-        const double rn = block_sum_fixed(cg.part_z + (size_t)v * nb, nb, scratch);
-        if (threadIdx.x == 0) cg_beta_update(cg, v, rn);
-    }
-    if (threadIdx.x == 0) cg_loop_control(cg, nvec);
-}
-
 }  // namespace
 }  // namespace bnf

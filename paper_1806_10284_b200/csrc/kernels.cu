@@ -833,18 +833,13 @@ __global__ void __launch_bounds__(R * N2) k_xpass_fast(double2* __restrict__ U, 
             v[u * N2 + k2] = cscale(x, s_);
         }
     if (CG) {
-        // (p, M p) partial of this CTA; the last CTA of the launch forms alpha
+        // (p, M p) partial of this CTA; k_cg_finish forms alpha after the pass
         // (read by the next pass, zadj)
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cg.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, sm);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;   // global over split (slab) launches
-        if (cg.ext_a) {
-            if (lin == 0 && threadIdx.x == 0) *cg.nb_x = nb;
-        } else if (cg_last_block(cg.counter + 0, gridDim.x * 3 * nvec_all, sm, lin)) {
-            cg_finish_alpha(cg, nb, nvec_all, sm);
-        }
+        if (lin == 0 && threadIdx.x == 0) *cg.nb_x = nb;   // alpha: k_cg_finish after this pass
     }
     fast::fft_mirror<N1, N2, -1, X>(v, t, w, sm, a.px.root2);
     if (ok) {
@@ -1031,11 +1026,7 @@ __global__ void __launch_bounds__(3 * W * N2) k_zadj_fast(const double2* __restr
     if (CG) {
         const int nb = gridDim.x * gridDim.y;
         cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, sm);
-        if (cg.ext) {
-            if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *cg.nb_z = nb;
-        } else if (cg_last_block(cg.counter + 1 + kCgGroups, gridDim.x * gridDim.y * gridDim.z, sm)) {
-            cg_finish_beta(cg, nb, gridDim.z, sm);
-        }
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *cg.nb_z = nb;   // beta: k_cg_finish
     }
 }
 

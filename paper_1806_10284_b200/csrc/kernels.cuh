@@ -69,7 +69,6 @@ struct CGFuse {
     double2* R;
     double* part_x;           // [nvec][partials]
     double* part_z;
-    unsigned int* counter;    // [2], zero between launches
     double* rr;
     double* pmp;
     double* alpha;
@@ -77,9 +76,7 @@ struct CGFuse {
     double* thr;
     int* active;
     int* nb_x;                         // partial counts per vector written by the producing passes
-    int* nb_z;                         //   (ext mode: reduced by k_cg_finish after the pass)
-    int ext;                           // 1: beta formed by k_cg_finish after zadj (no in-kernel election)
-    int ext_a;                         // 1: alpha formed by k_cg_finish after the (p, M p) pass
+    int* nb_z;                         //   (reduced by k_cg_finish after the pass)
     int* iter;                         // CG iterations done (device), or null
     int max_iter;
     int use_cond;                      // 1: set the CG graph's while-condition

@@ -260,16 +260,12 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     __syncthreads();   // D is reused by the next plane
     }   // planes
     if (CG) {
-        // per-CTA partials of (p, M p) for every vector; the last CTA of the launch forms alpha
+        // per-CTA partials of (p, M p) for every vector
         const int nvec = nslab / 3;
         const int nb = gridDim.x;
         if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
         __syncthreads();
-        if (cgf.ext_a) {
-            if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;
-        } else if (cg_last_block(cgf.counter + 0, nb, D)) {
-            cg_finish_alpha(cgf, nb, nvec, D);
-        }
+        if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;   // alpha: k_cg_finish after this pass
     }
 }
 
@@ -392,17 +388,12 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         }
     }
     if (CG) {
-        // this plane's (p, M p) partial; the last CTA of the launch forms alpha
+        // this plane's (p, M p) partial; alpha is formed by k_cg_finish after this pass
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        const int nvec_all = a.nvec_all > 0 ? a.nvec_all : (int)gridDim.y / 3;
         cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (cgf.ext_a) {
-            if (lin == 0 && tid == 0) *cgf.nb_x = nb;
-        } else if (cg_last_block(cgf.counter + 0, gridDim.x * 3 * nvec_all, D, lin)) {
-            cg_finish_alpha(cgf, nb, nvec_all, D);
-        }
+        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
     }
 }
 

@@ -422,7 +422,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
         BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
-        if (cg.ext_a) BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
@@ -438,7 +438,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
 }
 
 // CUDA graph of the whole CG loop: a device-side WHILE node whose body is one
-// CG iteration; the last CTA of the zadj pass sets the condition (any vector
+// CG iteration; the beta k_cg_finish after the zadj pass sets the condition (any vector
 // still active and iterations < max_inner, cgfuse.cuh).  No host round trip
 // per iteration.  Cached per (output block, nvec, operator version).
 int cg_graph(bnf_solver* s, const CGFuse& cg0, double2* R, double2* P, double2* U, double2* X, int nvec,
@@ -520,8 +520,8 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     CGFuse cg = s->cgf;
     cg.P = P;
     cg.R = R;
-    cg.ext = 1;   // beta by k_cg_finish after zadj (thousands of CTAs: no per-CTA fences)
-    cg.ext_a = 1;   // alpha by k_cg_finish after the (p, M p) pass (in-kernel election measured no faster)
+    // alpha / beta by k_cg_finish after the (p, M p) / (r, r) pass: the kernel boundary orders
+    // the partials (no per-CTA fences or last-CTA election; an election measured no faster)
     cg.nb_x = s->d_iter + 4;
     cg.nb_z = s->d_iter + 5;
     int it = 0;
@@ -543,7 +543,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
-                if (cg.ext_a) RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
+                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
                 RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
@@ -988,7 +988,6 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         char* c = b + 2 * 8 * per * sizeof(double);
         s->cgf.pmp = (double*)c;
         s->cgf.alpha = (double*)(c + 64 * sizeof(double));
-        s->cgf.counter = (unsigned int*)(c + 4 * 64 * sizeof(double));
         s->cgf.rr = s->cgs.rr;
         s->cgf.beta = s->cgs.beta;
         s->cgf.thr = s->cgs.thr;

@@ -16,7 +16,7 @@
 //
 // CG-fused variants (cg_solve_fused, solver.cu), per iteration:
 //   zfwd_cg : x += alpha_prev p;  p <- r + beta p;  U = Q_r-side of p
-//   zadj_cg : r -= alpha M p;  partial (r, r);  the last CTA forms beta
+//   zadj_cg : r -= alpha M p;  per-CTA partial (r, r); k_cg_finish forms beta
 // (the x update is deferred by one iteration so that zadj touches only U
 // and r; the final update is k_cg_xfinal).
 #include <cuda_runtime.h>
@@ -274,14 +274,10 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
         }
     }
     if (MODE == 1) {
-        // per-CTA partial of (r, r); the last CTA of the launch forms beta
+        // per-CTA partial of (r, r); beta is formed by k_cg_finish after this pass
         const int nb = gridDim.x * gridDim.y;
         cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, red);
-        if (cg.ext) {
-            if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb;
-        } else if (cg_last_block(cg.counter + 1 + kCgGroups, nb * gridDim.z, red)) {
-            cg_finish_beta(cg, nb, gridDim.z, red);
-        }
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb;
     }
 }
 
