@@ -78,7 +78,7 @@ struct ColS {   // per-column constants shared through smem
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
 template <int N1, int N2, int W, int MODE>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, BNF_Z_MINB)
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
