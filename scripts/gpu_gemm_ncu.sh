@@ -3,11 +3,11 @@
 TAG=${1:-gemm}
 set -x
 python paper_1806_10284_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
-timeout 1200 python -m pytest tests -m gpu -x -q -k "polish or residual or graph" > gpurun_out/pytest_$TAG.log 2>&1; echo pytest rc=$?
-tail -2 gpurun_out/pytest_$TAG.log
+true
+true
 CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu"
 $CMD > gpurun_out/prof_plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_gemm_(tn_partial|nn)" -s 60 -c 6 \
+    -k regex:"k_gemm_(tn_partial|nn)" -s ${SKIP:-60} -c 6 \
     -o gpurun_out/full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo ncu rc=$?
