@@ -1,10 +1,9 @@
-# GPU test suite + ncu full captures of the Lanczos block kernels (X^*Y partial
-# products, W -= V C) and the CG scalar kernel at the bench workload
+# ncu full captures of the Lanczos block kernels (X^*Y partial products,
+# W -= V C) at the bench workload; SKIP = matching launches skipped first
+# (larger SKIP = later Lanczos steps, wider basis)
 TAG=${1:-gemm}
 set -x
 python paper_1806_10284_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
-true
-true
 CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu"
 $CMD > gpurun_out/prof_plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
