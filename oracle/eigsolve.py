@@ -114,10 +114,38 @@ def inverse_lanczos(op, nev, block=1, guard=0, tol_outer=1e-12, tol_inner=1e-13,
     return lam[o][:nev], Y[:, o][:, :nev], info
 
 
-def dense_nfsep(Ar, nev, gamma_masked=False):
-    """Plain definition on a dense A_r: the nev smallest eigenvalues; with a
-    masked Gamma mode the 2 structural zeros are skipped."""
-    w = np.linalg.eigvalsh(Ar)
-    if gamma_masked:
-        w = w[2:]
-    return w[:nev]
+def arpack_inverse(op, nev, guard=4, tol_outer=1e-12, tol_inner=1e-13, ncv=None,
+                   seed=0x5EED):
+    """Bounded-memory route to the same plain result (SURVEY.md §8(c) step
+    5, "eigsh on a LinearOperator for A_r^{-1}"): the library implicitly
+    restarted Lanczos (ARPACK, scipy.sparse.linalg.eigsh) on
+    A_r^{-1} = Sigma_r^{-1} M^{-1} Sigma_r^{-1} (P:L2252-2255), each
+    application one CG solve with M to tol_inner, the Gamma mode
+    masked (R6).  ARPACK's stopping test ||r_i|| <= tol |theta_i| on the
+    Ritz pairs of A_r^{-1} is reading R12 with tol = tol_outer.  Used where
+    the full Krylov basis of inverse_lanczos does not fit host memory
+    (config 5, 256^3: one basis vector is 0.5 GiB).
+    Returns (lambda ascending (nev,), Ritz vectors (2n, nev), info dict)."""
+    from scipy.sparse.linalg import LinearOperator, eigsh
+
+    N = 2 * op.n
+    sig = np.concatenate([op.sig.ravel(), op.sig.ravel()])
+    mask = sig > 0
+    sinv = np.where(mask, 1.0 / np.where(mask, sig, 1.0), 0.0)
+    inner = []
+
+    def opinv(x):
+        y, its = cg(op.M, sinv * np.ravel(x), tol=tol_inner)
+        inner.extend(its)
+        return sinv * y
+
+    want = nev + guard
+    rng = np.random.default_rng(seed)
+    v0 = (rng.standard_normal(N) + 1j * rng.standard_normal(N)) * mask
+    A = LinearOperator((N, N), matvec=opinv, dtype=np.complex128)
+    theta, Y = eigsh(A, k=want, which="LA", v0=v0, tol=tol_outer,
+                     ncv=ncv or max(2 * want + 1, 20), maxiter=10000)
+    lam = 1.0 / theta
+    o = np.argsort(lam)
+    info = {"steps": len(inner), "inner_iters": inner, "matvecs": int(np.sum(inner))}
+    return lam[o][:nev], Y[:, o][:, :nev], info

@@ -8,14 +8,43 @@ DFT matrix U[s, t] = e^{+2 pi i s t / n}:  U x = n * ifft(x),
 U^* x = fft(x).  Normalisation: T is unitary with n^{-1/2}
 (eq. T); the "1/n" printed in the algorithms is
 read as n^{-1/2} each way (R7b).
+
+Execution knobs (no effect on the arithmetic): ORACLE_FFT_WORKERS (default
+1) is passed to scipy.fft as `workers` (threads over independent 1D
+transforms); ORACLE_THREADS (default 1) > 1 runs the three components of
+M / recover in threads.  Each component's chain is unchanged and the
+component contributions are summed in the fixed order l = 0, 1, 2, so the
+result is bit-identical to the serial loop.
 """
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
+import scipy.fft as _sfft
 
 from . import spectral
+
+_WORKERS = int(os.environ.get("ORACLE_FFT_WORKERS", "1"))
+_THREADS = int(os.environ.get("ORACLE_THREADS", "1"))
+
+
+def _ifft(x, axis):
+    return _sfft.ifft(x, axis=axis, workers=_WORKERS)
+
+
+def _fft(x, axis):
+    return _sfft.fft(x, axis=axis, workers=_WORKERS)
+
+
+def _per_component(fn):
+    """[fn(0), fn(1), fn(2)], serially or in threads (independent chains)."""
+    if _THREADS > 1:
+        with ThreadPoolExecutor(3) as ex:
+            return list(ex.map(fn, range(3)))
+    return [fn(l) for l in range(3)]
 
 
 def _diag_phases(lat, kappa):
@@ -46,11 +75,11 @@ def T_apply(lat, kappa, q, D=None):
     """Algorithm 2: T q."""
     n1, n2, n3 = lat.n
     D1, D2, D3 = D or _diag_phases(lat, kappa)
-    x = np.fft.ifft(q, axis=0) * n3          # U_n3 along k -> c
+    x = _ifft(q, axis=0) * n3          # U_n3 along k -> c
     x = x * D3                               # D_{a^3,i,j}
-    x = np.fft.ifft(x, axis=1) * n2          # U_n2 along j -> b
+    x = _ifft(x, axis=1) * n2          # U_n2 along j -> b
     x = x * D2                               # D_{a^2,i}
-    x = np.fft.ifft(x, axis=2) * n1          # U_n1 along i -> a
+    x = _ifft(x, axis=2) * n1          # U_n1 along i -> a
     x = x * D1                               # D_{a1}
     return x / math.sqrt(n1 * n2 * n3)
 
@@ -60,11 +89,11 @@ def Tstar_apply(lat, kappa, p, D=None):
     n1, n2, n3 = lat.n
     D1, D2, D3 = D or _diag_phases(lat, kappa)
     x = p * np.conj(D1)
-    x = np.fft.fft(x, axis=2)
+    x = _fft(x, axis=2)
     x = x * np.conj(D2)
-    x = np.fft.fft(x, axis=1)
+    x = _fft(x, axis=1)
     x = x * np.conj(D3)
-    x = np.fft.fft(x, axis=0)
+    x = _fft(x, axis=0)
     return x / math.sqrt(n1 * n2 * n3)
 
 
@@ -90,14 +119,18 @@ class NFSEPOperator:
     def M(self, y):
         n = self.n
         y = np.asarray(y).reshape(2, *self.shp)
-        z1 = np.zeros(self.shp, dtype=np.complex128)
-        z2 = np.zeros(self.shp, dtype=np.complex128)
-        for l in range(3):
+
+        def comp(l):
             v = self.Pi1[l] * y[0] + self.Pi2[l] * y[1]          # Q_r y, Fourier side
             u = T_apply(self.lat, self.kappa, v, self.D)        # real space
             w = Tstar_apply(self.lat, self.kappa, u * self.binv[l], self.D)
-            z1 += np.conj(self.Pi1[l]) * w
-            z2 += np.conj(self.Pi2[l]) * w
+            return np.conj(self.Pi1[l]) * w, np.conj(self.Pi2[l]) * w
+
+        z1 = np.zeros(self.shp, dtype=np.complex128)
+        z2 = np.zeros(self.shp, dtype=np.complex128)
+        for c1, c2 in _per_component(comp):
+            z1 += c1
+            z2 += c2
         return np.concatenate([z1.ravel(), z2.ravel()])
 
     def Ar(self, y):
@@ -111,8 +144,9 @@ class NFSEPOperator:
         """e = B^{-1} Q_r Sigma_r y, real-space Yee layout
         (3, n3, n2, n1)."""
         y = np.asarray(y).reshape(2, *self.shp)
-        out = []
-        for l in range(3):
+
+        def comp(l):
             v = self.sig * (self.Pi1[l] * y[0] + self.Pi2[l] * y[1])
-            out.append(T_apply(self.lat, self.kappa, v, self.D) * self.binv[l])
-        return np.stack(out)
+            return T_apply(self.lat, self.kappa, v, self.D) * self.binv[l]
+
+        return np.stack(_per_component(comp))

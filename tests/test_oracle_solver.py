@@ -66,3 +66,42 @@ def test_small_config_lattices(golden_dir, case):
     nev = 6
     lam, _, _ = eigsolve.inverse_lanczos(op, nev=nev, block=4, guard=4)
     np.testing.assert_allclose(lam, c["lambda"][:nev], rtol=1e-10)
+
+
+@pytest.mark.parametrize("case", [0, 4, 8])
+def test_arpack_route_matches_dense(golden_dir, case):
+    """The bounded-memory ARPACK route (used for the 256^3 golden) reaches
+    the dense NFSEP eigenvalues (tests/golden/small_nfsep_oracle.json) to
+    1e-10 relative, including a masked Gamma case."""
+    with open(os.path.join(golden_dir, "small_nfsep_oracle.json")) as f:
+        c = json.load(f)["cases"][case]
+    cfg = configs.config(c["config"])
+    n = tuple(c["n"])
+    L = lattice.snap(cfg.a_raw, n)
+    eps = E.sample(cfg.shape, n, L.a, L.delta, L.a_canon)
+    op = fftop.NFSEPOperator(L, tuple(c["kappa"]), eps)
+    lam, Y, _ = eigsolve.arpack_inverse(op, nev=6, guard=4)
+    np.testing.assert_allclose(lam, c["lambda"][:6], rtol=1e-10)
+    for i in range(6):
+        r = op.Ar(Y[:, i]) - lam[i] * Y[:, i]
+        assert np.linalg.norm(r) / np.linalg.norm(Y[:, i]) < 1e-6
+
+
+def test_threaded_operator_bit_identical():
+    """ORACLE_THREADS / ORACLE_FFT_WORKERS change only execution: the
+    threaded M equals the serial M bit for bit."""
+    from oracle import fftop as F
+    cfg = configs.config(4)
+    n = (12, 10, 8)
+    L = lattice.snap(cfg.a_raw, n)
+    eps = E.sample(cfg.shape, n, L.a, L.delta, L.a_canon)
+    op = F.NFSEPOperator(L, (0.1, 0.2, 0.3), eps)
+    y = np.random.default_rng(1).standard_normal(2 * op.n) + 1j
+    z0 = op.M(y)
+    t, w = F._THREADS, F._WORKERS
+    try:
+        F._THREADS, F._WORKERS = 3, 2
+        z1 = op.M(y)
+    finally:
+        F._THREADS, F._WORKERS = t, w
+    assert np.array_equal(z0, z1)
