@@ -130,10 +130,30 @@ def eps_for(cfg, lat):
 
 
 # ----------------------------------------------------------------- oracle arm
-def oracle_rate(cfg, seconds=15.0, max_matvecs=30, min_matvecs=2):
-    """Oracle (numpy, as it stands) matvecs/s on a bounded sample of the
-    same workload: A_r applications at the first k-point.  Returns
-    (rate, count, wall seconds, effective cores = process CPU time / wall)."""
+def host_info():
+    """CPU model, core count and library versions of the host the oracle runs on."""
+    import platform
+
+    import scipy
+    model = platform.processor() or "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count(), "numpy": np.__version__, "scipy": scipy.__version__,
+            "fft": "scipy.fft (pocketfft)", "python": platform.python_version()}
+
+
+def oracle_rate(cfg, seconds=15.0, max_matvecs=30, min_matvecs=2, threads=1, workers=1):
+    """Oracle (numpy/scipy, as it stands) matvecs/s on a bounded sample of
+    the same workload: A_r applications at the first k-point.  threads /
+    workers: the oracle's execution knobs (oracle/fftop.py ORACLE_THREADS,
+    ORACLE_FFT_WORKERS; bit-identical results).  Returns (rate, count, wall
+    seconds, effective cores = process CPU time / wall)."""
     from oracle import fftop, lattice as olat
     O = olat.snap(cfg.a_raw, cfg.n)
     eps = E.sample(cfg.shape, cfg.n, O.a, O.delta, O.a_canon)
@@ -143,16 +163,34 @@ def oracle_rate(cfg, seconds=15.0, max_matvecs=30, min_matvecs=2):
         kap = olat.kvec_reduce(O, cfg.kpoints[0])
     op = fftop.NFSEPOperator(O, kap, eps)
     y = np.random.default_rng(0).standard_normal(2 * O.nn) + 0j
-    t0 = time.perf_counter()
-    c0 = time.process_time()
-    cnt = 0
-    while cnt < max_matvecs and (cnt < min_matvecs or time.perf_counter() - t0 < seconds):
-        y = op.Ar(y)
-        y /= np.linalg.norm(y)
-        cnt += 1
-    dt = time.perf_counter() - t0
-    cores = (time.process_time() - c0) / dt
+    keep = (fftop._THREADS, fftop._WORKERS)
+    fftop._THREADS, fftop._WORKERS = threads, workers
+    try:
+        t0 = time.perf_counter()
+        c0 = time.process_time()
+        cnt = 0
+        while cnt < max_matvecs and (cnt < min_matvecs or time.perf_counter() - t0 < seconds):
+            y = op.Ar(y)
+            y /= np.linalg.norm(y)
+            cnt += 1
+        dt = time.perf_counter() - t0
+        cores = (time.process_time() - c0) / dt
+    finally:
+        fftop._THREADS, fftop._WORKERS = keep
     return cnt / dt, cnt, dt, cores
+
+
+def cpu_baseline_pair(cfg, seconds=12.0):
+    """The oracle single-threaded and on all host cores (3 component threads x
+    nproc/3 FFT workers), SURVEY §8(d).  Reported as a baseline, not a target."""
+    nproc = os.cpu_count() or 1
+    r1, c1, d1, co1 = oracle_rate(cfg, seconds=seconds, max_matvecs=20)
+    ra, ca, da, coa = oracle_rate(cfg, seconds=seconds, max_matvecs=40, threads=3, workers=max(1, nproc // 3))
+    return {"value": ra, "unit": "matvecs/s", "cores": round(coa, 2), "kind": "oracle",
+            "sample": "%d oracle A_r applications at %s, k-point 1 (scipy.fft, 3 component threads x %d FFT "
+                      "workers, %.1f s)" % (ca, cfg.name, max(1, nproc // 3), da),
+            "single_thread": {"value": r1, "cores": round(co1, 2), "applications": c1, "seconds": round(d1, 2)},
+            "host": host_info(), "note": "baseline, not a target (plain fp64 NumPy/SciPy oracle)"}
 
 
 def run_reference(args, rank, world):
@@ -170,14 +208,15 @@ def run_reference(args, rank, world):
         tt += dt
         cores.append(co)
     v = total / tt
-    sample = "%d oracle A_r applications (numpy FFT) at %s, %d steps of <= 6" % (total, cfg.name, args.steps)
+    sample = "%d oracle A_r applications (scipy.fft, 1 thread) at %s, %d steps of <= 6" % (total, cfg.name,
+                                                                                           args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "matvecs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic", "config": {"workload": cfg.name, "grid": list(cfg.n)},
         "cpu_baseline": {"value": v, "unit": "matvecs/s", "cores": round(max(cores), 2), "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": v, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,9 +238,20 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun (rank 0 prints the line)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.run(cmd).returncode)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d (launch one process per GPU)" % (args.gpus, world))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -245,6 +295,7 @@ def main():
     mv = 0
     launches = 0
     stats = []
+    lams = []
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for s in range(args.steps):
@@ -252,6 +303,7 @@ def main():
             mv += st["matvecs"]
             launches += st["kernel_launches"]
             stats.append(st)
+            lams.append((kidx(args.warmup + s), lam))
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -349,9 +401,18 @@ def main():
     matvec_bytes = sum(PASS_BYTES[k](n) * vecs(k) for k in ktimes if k in PASS_BYTES)
     cpu = None
     if not args.no_cpu and world == 1:   # the oracle baseline is timed at N = 1 only
-        r, c, dt, co = oracle_rate(cfg)
-        cpu = {"value": r, "unit": "matvecs/s", "cores": round(co, 2), "kind": "oracle",
-               "sample": "%d oracle A_r applications at %s, k-point 1 (numpy FFT, %.1f s)" % (c, cfg.name, dt)}
+        cpu = cpu_baseline_pair(cfg)
+    # timed k-points with an oracle golden (scripts/make_golden_full.py): eigenvalue deviation
+    devs = []
+    for ki, lam in lams:
+        gp = os.path.join(ROOT, "tests", "golden", "full_c%d_k%d_oracle.json" % (args.config, ki))
+        if os.path.exists(gp):
+            with open(gp) as f:
+                g = json.load(f)
+            gl = np.asarray(g["lambda"][:nev])
+            devs.append(float(np.max(np.abs(np.asarray(lam[:len(gl)]) - gl) / gl)))
+    golden = {"timed_kpoints_with_golden": len(devs), "timed_kpoints": len(lams),
+              "max_rel_dev_vs_oracle": max(devs) if devs else None}
     line = {
         "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -366,6 +427,7 @@ def main():
                             if matvec_ms else None, "share_of_step": matvec_ms / ms_prof,
                             "profiled_step_ms": ms_prof, "profiled_matvecs": mv_prof},
         "roofline": roof,
+        "golden_check": golden,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

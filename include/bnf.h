@@ -105,6 +105,12 @@ void bnf_lattice_destroy(bnf_lattice* lat);
    canonical vectors.  Host-only. */
 int bnf_kvec_reduce(const bnf_lattice* lat, const double K_cart[3], double kappa[3]);
 
+/* Reduced Bloch numbers given in the labelling of a_raw (kappa_raw_l =
+   K . a_raw_l / 2 pi) -> the canonical labelling the solver uses: canonical
+   vector l is raw vector perm[l] (cyclic relabel, longest first) and
+   kappa_3 changes sign when a3 was negated (DESIGN R10).  Host-only. */
+int bnf_kappa_canonical(const bnf_lattice* lat, const double kappa_raw[3], double kappa[3]);
+
 /* Yee points of component comp (0, 1, 2) at which B_comp is sampled
    (the edge midpoints x(a+1/2,b,c), x(a,b+1/2,c), x(a,b,c+1/2)
    of the grid of the snapped lattice).  xyz: HOST, n1*n2*n3 rows
@@ -125,7 +131,10 @@ typedef struct {
     void* stream;               /* cudaStream_t to issue work on; NULL = legacy default stream */
     double tol_outer;           /* 1e-12: Ritz relative residual of A_r^{-1} (DESIGN R12) */
     double tol_inner;           /* 1e-13: CG relative residual ||r|| <= tol ||c|| */
-    int max_outer;              /* max block-Lanczos steps */
+    int max_outer;              /* max block-Lanczos steps; 0 (default) = auto:
+                                   max(60, 12 ceil((nev + guard) / block)), capped by the NFSEP
+                                   dimension.  BNF_EINVAL from bnf_solve if max_outer * block
+                                   < nev + guard.  The basis grows on demand (VMM mapping). */
     int max_inner;              /* max CG iterations per solve */
     int block;                  /* Lanczos block size b >= 1 (DESIGN R13) */
     int guard;                  /* extra Ritz pairs converged beyond nev */
@@ -154,6 +163,8 @@ typedef struct {
     double max_residual;        /* max_i ||A_r y_i - lambda_i y_i|| / ||y_i|| of the returned pairs */
     double seconds;             /* wall time of the call */
     int polish_steps;           /* extra inverse-iteration + Rayleigh-Ritz steps taken for res_tol */
+    int polish_failed;          /* 1 if a polish step's block was rank deficient (CholQR failed): the
+                                   previous Ritz pairs were kept and polishing stopped */
 } bnf_stats;
 
 /* Create a solver for a lattice on opts->device.  Allocates device memory
@@ -176,6 +187,14 @@ int bnf_set_kappa(bnf_solver* s, const double kappa[3]);
    complex128 [b][2][n] (Fourier layout).  out may not alias y.  Uses the
    kappa of the last bnf_set_kappa / bnf_solve. */
 int bnf_apply_Ar(bnf_solver* s, const void* y, void* out, int b, int op);
+
+/* Inner solve hook: x = M^{-1} c by the
+   solver's CG (CG-fused passes, CUDA-graph loop unless profiling is on) for b
+   right-hand sides, stopping per column at ||r|| <= tol_inner ||c|| or after
+   max_iter iterations.  c, x: DEVICE complex128 [b][2][n], caller-owned, may
+   not alias.  *iters (may be NULL) = iterations run.  Uses the kappa of the
+   last bnf_set_kappa.  BNF_ESTATE before bnf_set_epsilon / bnf_set_kappa. */
+int bnf_cg_solve(bnf_solver* s, const void* c, void* x, int b, int max_iter, int* iters);
 
 /* Solve: nev smallest nonzero eigenvalues of the GEP at
    kappa, ascending, written to lambda[nev] (HOST).  Eigenvectors stay on the

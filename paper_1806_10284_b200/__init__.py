@@ -51,7 +51,7 @@ class Stats(C.Structure):
     _fields_ = [("outer_steps", C.c_int), ("converged", C.c_int), ("inner_iters", C.c_longlong),
                 ("matvecs", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("max_ritz_residual", C.c_double), ("max_residual", C.c_double), ("seconds", C.c_double),
-                ("polish_steps", C.c_int)]
+                ("polish_steps", C.c_int), ("polish_failed", C.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -65,6 +65,8 @@ _sigs = {
     "bnf_lattice_create": [C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(_P)],
     "bnf_lattice_query": [_P, C.POINTER(LatticeInfo)],
     "bnf_kvec_reduce": [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bnf_kappa_canonical": [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bnf_cg_solve": [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_int)],
     "bnf_yee_points": [_P, C.c_int, C.c_int, C.POINTER(C.c_double)],
     "bnf_solver_create": [_P, C.POINTER(Opts), C.POINTER(_P)],
     "bnf_set_epsilon": [_P, _P, C.c_int],
@@ -91,7 +93,8 @@ _lib.bnf_opts_default.restype = None
 
 FRAME_SNAPPED, FRAME_ORIGINAL = 0, 1
 
-EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce", "bnf_yee_points",
+EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce",
+           "bnf_kappa_canonical", "bnf_cg_solve", "bnf_yee_points",
            "bnf_opts_default", "bnf_solver_create", "bnf_solver_destroy", "bnf_set_epsilon", "bnf_set_kappa",
            "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile", "bnf_phase_counters",
            "bnf_last_error", "bnf_version", "bnf_host_herm_eig"]
@@ -151,9 +154,9 @@ class Lattice:
         return out
 
     def kappa_from_raw(self, kappa_raw):
-        k = [float(kappa_raw[self.perm[l]]) for l in range(3)]
-        k[2] *= self.sign3
-        return tuple(k)
+        out = _D3()
+        _check(_lib.bnf_kappa_canonical(self._h, _D3(*[float(x) for x in kappa_raw]), out))
+        return tuple(out)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -192,6 +195,12 @@ class Solver:
     def apply_Ar(self, y, out, b, op=OP_AR):
         """y, out: CUDA complex128 torch tensors of b*2n elements."""
         _check(_lib.bnf_apply_Ar(self._h, _ptr(y), _ptr(out), int(b), int(op)))
+
+    def cg_solve(self, c, x, b, max_iter):
+        """x = M^{-1} c by the solver's CG (c, x: CUDA complex128 tensors of b*2n)."""
+        it = C.c_int()
+        _check(_lib.bnf_cg_solve(self._h, _ptr(c), _ptr(x), int(b), int(max_iter), C.byref(it)))
+        return it.value
 
     def solve(self, kappa, nev, allow_noconv=False):
         lam = np.zeros(nev)

@@ -6,6 +6,8 @@
 //   a6  batched CG on M = Q_r^* B^{-1} Q_r          (cg_solve)
 //   a7  block inverse Lanczos with full reorthogonalisation         (bnf_solve)
 //   a8  Rayleigh-Ritz on A_r, residuals, E-field recovery           (refine / bnf_eigvecs)
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -108,6 +110,138 @@ struct DevBuf {
     }
 };
 
+// Device buffer that grows in place: a virtual address range is reserved once
+// for the largest size the caller may need (CUDA virtual memory management:
+// cuMemAddressReserve) and physical memory is mapped behind it in chunks as
+// the buffer grows (cuMemCreate + cuMemMap).  The Krylov basis uses it: its
+// final size (m + 1 blocks of b vectors of 2n complex128) is unknown until
+// the iteration stops, 256^3 vectors are 0.5 GiB each, and growth by copy
+// would need old + new at once.  Driver entry points come through
+// cudaGetDriverEntryPoint (no libcuda link dependency).
+struct Vmm {
+    PFN_cuMemAddressReserve reserve = nullptr;
+    PFN_cuMemAddressFree free_va = nullptr;
+    PFN_cuMemCreate create = nullptr;
+    PFN_cuMemRelease release = nullptr;
+    PFN_cuMemMap map = nullptr;
+    PFN_cuMemUnmap unmap = nullptr;
+    PFN_cuMemSetAccess access = nullptr;
+    PFN_cuMemGetAllocationGranularity gran = nullptr;
+    bool ok = false;
+    static const Vmm& get() {
+        static Vmm v = [] {
+            Vmm x;
+            auto ld = [](const char* name, void** fn) {
+                cudaDriverEntryPointQueryResult q;
+                return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                       q == cudaDriverEntryPointSuccess && *fn != nullptr;
+            };
+            x.ok = ld("cuMemAddressReserve", (void**)&x.reserve) && ld("cuMemAddressFree", (void**)&x.free_va) &&
+                   ld("cuMemCreate", (void**)&x.create) && ld("cuMemRelease", (void**)&x.release) &&
+                   ld("cuMemMap", (void**)&x.map) && ld("cuMemUnmap", (void**)&x.unmap) &&
+                   ld("cuMemSetAccess", (void**)&x.access) &&
+                   ld("cuMemGetAllocationGranularity", (void**)&x.gran);
+            return x;
+        }();
+        return v;
+    }
+};
+
+struct GrowBuf {
+    CUdeviceptr base = 0;
+    size_t reserved = 0, mapped = 0, granule = 0;
+    int dev = 0;
+    std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks;
+    ~GrowBuf() { clear(); }
+    void clear() {
+        const Vmm& v = Vmm::get();
+        if (!v.ok) return;
+        size_t off = 0;
+        for (auto& c : chunks) {
+            v.unmap(base + off, c.second);
+            v.release(c.first);
+            off += c.second;
+        }
+        chunks.clear();
+        mapped = 0;
+        if (base) v.free_va(base, reserved);
+        base = 0;
+        reserved = 0;
+    }
+    // reserve address space for `bytes` (drops the contents if it must re-reserve)
+    int reserve(size_t bytes, int device) {
+        const Vmm& v = Vmm::get();
+        if (!v.ok) {
+            set_error("CUDA virtual memory management entry points unavailable");
+            return BNF_ECUDA;
+        }
+        if (base && bytes <= reserved && device == dev) return BNF_OK;
+        clear();
+        dev = device;
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = dev;
+        if (v.gran(&granule, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || granule == 0) {
+            set_error("cuMemGetAllocationGranularity failed");
+            return BNF_ECUDA;
+        }
+        const size_t r = ((bytes + granule - 1) / granule) * granule;
+        if (v.reserve(&base, r, 0, 0, 0) != CUDA_SUCCESS) {
+            base = 0;
+            set_error("cuMemAddressReserve failed");
+            return BNF_ENOMEM;
+        }
+        reserved = r;
+        return BNF_OK;
+    }
+    // map physical memory so that [base, base + bytes) is usable
+    int ensure(size_t bytes) {
+        if (bytes <= mapped) return BNF_OK;
+        if (bytes > reserved) {
+            set_error("GrowBuf: request beyond the reserved range");
+            return BNF_EINVAL;
+        }
+        const Vmm& v = Vmm::get();
+        // grow by at least 1/4 of what is mapped (fewer, larger chunks), within the reservation
+        size_t want = std::max(bytes - mapped, mapped / 4);
+        want = ((want + granule - 1) / granule) * granule;
+        want = std::min(want, reserved - mapped);
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = dev;
+        CUmemGenericAllocationHandle h;
+        if (v.create(&h, want, &prop, 0) != CUDA_SUCCESS) {
+            set_error("out of device memory growing the Krylov basis (" + std::to_string((mapped + want) >> 20) +
+                      " MiB)");
+            return BNF_ENOMEM;
+        }
+        if (v.map(base + mapped, want, 0, h, 0) != CUDA_SUCCESS) {
+            v.release(h);
+            set_error("cuMemMap failed");
+            return BNF_ECUDA;
+        }
+        CUmemAccessDesc acc = {};
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = dev;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (v.access(base + mapped, want, &acc, 1) != CUDA_SUCCESS) {
+            v.unmap(base + mapped, want);
+            v.release(h);
+            set_error("cuMemSetAccess failed");
+            return BNF_ECUDA;
+        }
+        chunks.push_back({h, want});
+        mapped += want;
+        return BNF_OK;
+    }
+    template <class T>
+    T* as() const {
+        return reinterpret_cast<T*>(base);
+    }
+};
+
 }  // namespace
 
 // ------------------------------------------------------------- profiler
@@ -206,7 +340,8 @@ struct bnf_solver {
     int graph_kernels_per_iter = 0;
     long long graph_calls = 0;
     DevBuf hroot;             // e^{i pi k / n3}
-    DevBuf V, Wb, AZ, Yv;  // Lanczos basis, work block, A_r * Ritz, Ritz vectors
+    GrowBuf V;             // Lanczos basis (grows with the iteration, VMM-backed)
+    DevBuf Wb, AZ, Yv;     // work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
     int nev_last = 0;
     int prev_want = 0;   // Ritz vectors of the last solve kept in Yv (warm start)
@@ -781,6 +916,20 @@ int bnf_kvec_reduce(const bnf_lattice* lat, const double K[3], double kappa[3]) 
     return BNF_OK;
 }
 
+int bnf_kappa_canonical(const bnf_lattice* lat, const double kappa_raw[3], double kappa[3]) {
+    if (!lat || !kappa_raw || !kappa) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    // canonical vector l is raw vector perm[l]; a3 negated when sign3 = -1 (R10)
+    const Lattice& L = lat->L;
+    double k[3];
+    for (int l = 0; l < 3; ++l) k[l] = kappa_raw[L.perm[l]];
+    k[2] *= (double)L.sign3;
+    for (int l = 0; l < 3; ++l) kappa[l] = k[l];
+    return BNF_OK;
+}
+
 int bnf_yee_points(const bnf_lattice* lat, int comp, int frame, double* xyz) {
     if (!lat || !xyz) {
         set_error("NULL argument");
@@ -829,7 +978,7 @@ void bnf_opts_default(bnf_opts* o) {
     o->stream = nullptr;
     o->tol_outer = 1e-12;
     o->tol_inner = 1e-13;
-    o->max_outer = 60;
+    o->max_outer = 0;   // auto: max(60, 12 ceil((nev + guard) / block)) steps
     o->max_inner = 2000;
     o->block = 4;
     o->guard = 4;
@@ -850,7 +999,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     bnf_opts o;
     bnf_opts_default(&o);
     if (opts) o = *opts;
-    if (o.block < 1 || o.block > 8 || o.guard < 0 || o.max_outer < 1 || o.max_inner < 1) {
+    if (o.block < 1 || o.block > 8 || o.guard < 0 || o.max_outer < 0 || o.max_inner < 1) {
         set_error("invalid solver options (block must be 1..8)");
         return BNF_EINVAL;
     }
@@ -1100,6 +1249,38 @@ int bnf_apply_Ar(bnf_solver* s, const void* y, void* out, int b, int op) {
     return BNF_OK;
 }
 
+int bnf_cg_solve(bnf_solver* s, const void* c, void* x, int b, int max_iter, int* iters) {
+    if (!s || !c || !x || b < 1 || b > 64 || max_iter < 1) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    if (!s->eps_set || !s->kappa_set) {
+        set_error("bnf_set_epsilon and bnf_set_kappa must precede bnf_cg_solve");
+        return BNF_ESTATE;
+    }
+    TRY(autotune_plane(s, b));
+    const int keep = s->o.max_inner;
+    s->o.max_inner = max_iter;
+    s->kver++;   // cached CG graphs carry the iteration cap
+    int it = -1;
+    CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
+    const long long g0 = s->graph_calls;
+    const int rc = s->fused_ok ? cg_solve_fused(s, (const double2*)c, (double2*)x, b, &it)
+                               : cg_solve(s, (const double2*)c, (double2*)x, b, &it);
+    s->o.max_inner = keep;
+    s->kver++;
+    if (rc != BNF_OK) return rc;
+    CK(cudaStreamSynchronize(s->st));
+    if (s->prof.on) s->prof.flush();
+    if (s->graph_calls > g0) {   // iterations counted on the device inside the graph
+        int h[3];
+        CK(cudaMemcpy(h, s->d_iter, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+        it = h[0];
+    }
+    if (iters) *iters = it;
+    return BNF_OK;
+}
+
 int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf_stats* stats) {
     auto t0 = std::chrono::steady_clock::now();
     if (!s || !kappa || !lambda || nev < 1) {
@@ -1125,33 +1306,25 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         set_error("nev + guard exceeds the NFSEP dimension");
         return BNF_EINVAL;
     }
-    const int maxsteps = std::max(1, std::min<int>(s->o.max_outer, (int)((dof + b - 1) / b)));
-    const size_t vbytes = (size_t)N * sizeof(double2);
-    CK(s->V.ensure(vbytes * (size_t)b * (maxsteps + 1)));
-    CK(s->Wb.ensure(vbytes * b));
-    CK(s->cgx.ensure(vbytes * b));
-    double2* V = s->V.as<double2>();
-    double2* W = s->Wb.as<double2>();
-    // start block: seeded counter-based normals, Gamma mode masked (R6)
-    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st));
-    if (s->o.warm && s->prev_want > 0) {
-        // Warm start (DESIGN R17): start block = fixed pseudo-random combinations of
-        // the previous solve's Ritz vectors (neighbouring k on the path) plus 1e-3 of
-        // the random block; Gamma mode masked.  Only the start block changes; the
-        // iteration, its tolerance and the returned eigenpairs are as before.
-        const int pw = s->prev_want;
-        std::vector<cd> Wm((size_t)pw * b);
-        unsigned long long h = 0x9E3779B97F4A7C15ull;
-        for (auto& x : Wm) {
-            h ^= h >> 33;
-            h *= 0xff51afd7ed558ccdull;
-            h ^= h >> 33;
-            x = cd(((double)(h >> 11) / 9007199254740992.0) - 0.5, 0.0);
-        }
-        TRY(gemm_nn_host(s, s->Yv.as<double2>(), pw, Wm, b, V, 1.0, 1e-3));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st));
+    // Lanczos step cap: opts.max_outer, or (0 = auto) enough steps for the wanted
+    // pairs with a margin that scales with ceil(want / b) -- single-vector runs
+    // (b = 1) need several times more steps than b = 4 for the same pairs
+    const long long cap_dof = (dof + b - 1) / b;
+    const int auto_steps = std::max(60, 12 * ((want + b - 1) / b));
+    const int maxsteps = (int)std::max<long long>(1, std::min<long long>(s->o.max_outer > 0 ? s->o.max_outer : auto_steps,
+                                                                       cap_dof));
+    if ((long long)maxsteps * b < want) {
+        set_error("max_outer * block < nev + guard: the Krylov basis cannot hold the wanted pairs");
+        return BNF_EINVAL;
     }
+    const size_t vbytes = (size_t)N * sizeof(double2);
+    // basis: address space for every step, physical memory mapped as it grows
+    TRY(s->V.reserve(vbytes * (size_t)b * (maxsteps + 1), s->o.device));
+    TRY(s->V.ensure(vbytes * (size_t)b * 2));
+    CK(s->cgx.ensure(vbytes * b));
+    // small device scratch: gram_host / gemm_nn_host stage p x 8 blocks at offset 64
+    CK(s->small.ensure((size_t)(64 + 8 * std::max<long long>((long long)(maxsteps + 1) * b, want)) * sizeof(double2)));
+    double2* V = s->V.as<double2>();
     bool ok = true;
     std::vector<cd> R0;
     TRY(chol_qr2(s, V, b, R0, ok));
@@ -1167,16 +1340,25 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     double maxres = 0.0;
     for (int step = 0; step < maxsteps; ++step) {
         double2* Vj = V + (size_t)step * b * N;
+        TRY(s->V.ensure(vbytes * (size_t)b * (step + 2)));
+        double2* W = V + (size_t)(step + 1) * b * N;   // next block, built in place
         TRY(apply_Ar_inv(s, Vj, W, b));  // W = A_r^{-1} V_j
         // full reorthogonalisation (classical Gram-Schmidt against all of V) with the
         // DGKS / Kahan-Parlett "twice is enough" test: the second pass runs unless the
         // first kept every column's norm above 1/sqrt(2) of its value (norm after the
-        // pass from Pythagoras, V orthonormal); accumulate the projections
+        // pass from Pythagoras, V orthonormal); accumulate the projections.  Pass 1
+        // takes [V_0..V_step | W]^* W in one Gram: its last b rows are G0 = W^* W.
         const int p = (step + 1) * b;
         std::vector<cd> Hacc((size_t)p * b, 0.0), H, G0;
-        TRY(gram_host(s, W, b, W, b, G0));
         for (int pass = 0; pass < 2; ++pass) {
-            TRY(gram_host(s, V, p, W, b, H));
+            if (pass == 0) {
+                std::vector<cd> HG;
+                TRY(gram_host(s, V, p + b, W, b, HG));
+                H.assign(HG.begin(), HG.begin() + (size_t)p * b);
+                G0.assign(HG.begin() + (size_t)p * b, HG.end());
+            } else {
+                TRY(gram_host(s, V, p, W, b, H));
+            }
             TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
             for (size_t t = 0; t < H.size(); ++t) Hacc[t] += H[t];
             if (pass == 0 && s->o.reorth_once_ok) {
@@ -1221,7 +1403,6 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         As.push_back(A);
         Bs.push_back(Rn);
         m = step + 1;
-        RUN("copy", launch_copy(V + (size_t)(step + 1) * b * N, W, N * b, s->st));
         // block tridiagonal T_m and its eigen-decomposition
         const int mb = m * b;
         std::vector<cd> T((size_t)mb * mb, 0.0);
@@ -1280,22 +1461,28 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     std::vector<double> lam(want);
     for (int c = 0; c < want; ++c) lam[c] = 1.0 / theta[c];
     double maxr_ar = -1.0;
-    int polish = 0;
+    int polish = 0, polish_failed = 0;
     if (s->o.refine >= 1) for (int pass = 0;; ++pass) {
         // Rayleigh-Ritz of A_r on span(Y) (DESIGN R15); a step of subspace
         // (inverse) iteration first when refine >= 2, and again while the
         // explicit residual of a returned pair exceeds res_tol (DESIGN R19).
-        if (s->o.refine >= 2 || pass > 0) {
-            for (int c0 = 0; c0 < want; c0 += b) {
-                const int qc = std::min(b, want - c0);
-                TRY(apply_Ar_inv(s, Y + (size_t)c0 * N, s->cgx.as<double2>(), qc));
-                RUN("copy", launch_copy(Y + (size_t)c0 * N, s->cgx.as<double2>(), N * qc, s->st));
-            }
-            std::vector<cd> Rq;
-            TRY(chol_qr2(s, Y, want, Rq, ok));
-        }
         CK(s->AZ.ensure(vbytes * want));
         double2* AZ = s->AZ.as<double2>();
+        if (s->o.refine >= 2 || pass > 0) {
+            // subspace inverse iteration into AZ; adopted only if its Cholesky-QR
+            // succeeds (a rank-deficient block keeps the previous Y and lambda)
+            for (int c0 = 0; c0 < want; c0 += b) {
+                const int qc = std::min(b, want - c0);
+                TRY(apply_Ar_inv(s, Y + (size_t)c0 * N, AZ + (size_t)c0 * N, qc));
+            }
+            std::vector<cd> Rq;
+            TRY(chol_qr2(s, AZ, want, Rq, ok));
+            if (!ok) {
+                polish_failed = 1;
+                break;
+            }
+            RUN("copy", launch_copy(Y, AZ, N * want, s->st));
+        }
         for (int c0 = 0; c0 < want; c0 += b) {
             const int qc = std::min(b, want - c0);
             TRY(apply_op(s, Y + (size_t)c0 * N, AZ + (size_t)c0 * N, qc, BNF_OP_AR));
@@ -1358,6 +1545,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         stats->max_ritz_residual = maxres;
         stats->max_residual = maxr_ar;
         stats->polish_steps = polish;
+        stats->polish_failed = polish_failed;
         stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     if (!converged) {

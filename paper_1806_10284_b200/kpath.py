@@ -14,6 +14,13 @@ gathered at the end.  This module holds only host logic:
 * ``run_path``    -- drive a ``solve(kappa) -> (lam, stats)`` callable over
                      this rank's share, with per-k retry and a JSONL
                      checkpoint (resume skips finished k, SURVEY §5);
+* ``StealQueue``  -- dynamic balancing on top of the LPT shares: every rank
+                     walks its own share front to back through an atomic
+                     per-rank cursor in the process group's key-value store,
+                     and a rank whose share is exhausted takes the next
+                     unclaimed k of the rank with the most work left (each k
+                     is claimed exactly once; owners keep contiguous runs,
+                     so warm starts stay local);
 * ``gather``      -- merge every rank's records into path order
                      (torch.distributed object gather; gloo or nccl).
 """
@@ -56,6 +63,57 @@ def assign(kappas, world, costs=None):
     return [sorted(s) for s in share]
 
 
+class StealQueue:
+    """Exactly-once k claiming with work stealing (see module docstring).
+    ``store``: a torch.distributed Store (``add`` is atomic across ranks), or
+    None for a single process.  ``shares``: the LPT shares (``assign``)."""
+
+    def __init__(self, shares, rank, store=None, prefix="kpath"):
+        self.shares = [list(s) for s in shares]
+        self.rank = rank
+        self.store = store
+        self.prefix = prefix
+        self._local = [0] * len(self.shares)
+
+    def _add(self, r, inc):
+        if self.store is None:
+            v = self._local[r]
+            self._local[r] += inc
+            return v + inc
+        return int(self.store.add("%s/cursor%d" % (self.prefix, r), inc))
+
+    def _claim(self, r):
+        pos = self._add(r, 1) - 1
+        return self.shares[r][pos] if pos < len(self.shares[r]) else None
+
+    def __iter__(self):
+        while True:
+            i = self._claim(self.rank)
+            if i is not None:
+                yield i
+                continue
+            # own share exhausted: help the rank with the most unclaimed k
+            left = [(len(s) - self._add(r, 0), r) for r, s in enumerate(self.shares) if r != self.rank]
+            left = [x for x in left if x[0] > 0]
+            if not left:
+                return
+            _, victim = max(left)
+            i = self._claim(victim)
+            if i is not None:
+                yield i
+
+
+def run_meta(nev, eps=None, **opts):
+    """Identity of a run for checkpoint reuse: nev, a hash of eps, options."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(json.dumps({"nev": int(nev), **{k: opts[k] for k in sorted(opts)}}, default=str).encode())
+    if eps is not None:
+        import numpy as np
+        h.update(np.ascontiguousarray(eps).tobytes())
+    return h.hexdigest()[:16]
+
+
 @dataclass
 class KRecord:
     index: int
@@ -66,23 +124,33 @@ class KRecord:
     rank: int = 0
     attempts: int = 1
     seconds: float = 0.0
+    meta: str = ""              # run_meta() of the run that produced it
 
     def to_json(self):
         return json.dumps({"index": self.index, "kappa": list(self.kappa), "status": self.status,
                            "lam": list(self.lam), "stats": self.stats, "rank": self.rank,
-                           "attempts": self.attempts, "seconds": self.seconds})
+                           "attempts": self.attempts, "seconds": self.seconds, "meta": self.meta})
 
     @staticmethod
     def from_json(line):
         d = json.loads(line)
         return KRecord(d["index"], tuple(d["kappa"]), d["status"], d["lam"], d["stats"], d["rank"],
-                       d["attempts"], d["seconds"])
+                       d["attempts"], d["seconds"], d.get("meta", ""))
 
 
-def load_checkpoint(path):
-    """Finished records of a previous run (status ok or noconv), by k index."""
+def load_checkpoint(paths, kappas=None, meta=None):
+    """Finished records of previous runs (status ok or noconv), by k index.
+    ``paths``: one JSONL path or a list (every rank's file, so a resume with
+    another world size or stealing pattern still finds each finished k).  A
+    record is reused only if its kappa equals ``kappas[index]`` and its
+    ``meta`` equals ``meta`` (when given): a changed path, nev, eps or
+    option set is never served from a stale checkpoint."""
+    if isinstance(paths, str) or paths is None:
+        paths = [paths]
     done = {}
-    if path and os.path.exists(path):
+    for path in paths:
+        if not path or not os.path.exists(path):
+            continue
         with open(path) as f:
             for line in f:
                 line = line.strip()
@@ -90,22 +158,31 @@ def load_checkpoint(path):
                     continue
                 try:
                     r = KRecord.from_json(line)
-                except (ValueError, KeyError):
+                except (ValueError, KeyError, TypeError):
                     continue   # torn last line of an interrupted run
-                if r.status in ("ok", "noconv"):
-                    done[r.index] = r
+                if r.status not in ("ok", "noconv"):
+                    continue
+                if meta is not None and r.meta != meta:
+                    continue
+                if kappas is not None and (r.index >= len(kappas) or
+                                           tuple(float(x) for x in kappas[r.index]) != tuple(r.kappa)):
+                    continue
+                done[r.index] = r
     return done
 
 
-def run_path(solve, kappas, indices, rank=0, checkpoint=None, retries=1, clock=time.perf_counter):
-    """Solve the k-points ``indices`` (this rank's share) with ``solve``.
+def run_path(solve, kappas, indices, rank=0, checkpoint=None, retries=1, clock=time.perf_counter, meta="",
+             resume_from=None):
+    """Solve the k-points ``indices`` (this rank's share, or a StealQueue)
+    with ``solve``.
 
     ``solve(kappa)`` returns ``(lam, stats_dict)``; ``stats_dict["rc"]`` may
     mark non-convergence (6 = BNF_ENOCONV).  An exception is retried
     ``retries`` times and then recorded as ``failed`` (the path continues).
-    With ``checkpoint`` (a per-rank JSONL path) finished k are skipped and
-    new records are appended as they complete."""
-    done = load_checkpoint(checkpoint)
+    With ``checkpoint`` (a per-rank JSONL path) new records are appended as
+    they complete, and k finished by a previous run with the same ``meta``
+    and kappa (in ``checkpoint`` or any file of ``resume_from``) are skipped."""
+    done = load_checkpoint(list(resume_from or []) + [checkpoint], kappas, meta)
     out = []
     fh = open(checkpoint, "a") if checkpoint else None
     try:
@@ -120,10 +197,11 @@ def run_path(solve, kappas, indices, rank=0, checkpoint=None, retries=1, clock=t
                 try:
                     lam, st = solve(kap)
                     status = "noconv" if st.get("rc", 0) == 6 else "ok"
-                    rec = KRecord(i, kap, status, [float(x) for x in lam], dict(st), rank, attempt, clock() - t0)
+                    rec = KRecord(i, kap, status, [float(x) for x in lam], dict(st), rank, attempt, clock() - t0,
+                                  meta)
                     break
                 except Exception as e:  # noqa: BLE001 -- recorded, path continues
-                    rec = KRecord(i, kap, "failed", [], {"error": str(e)}, rank, attempt, clock() - t0)
+                    rec = KRecord(i, kap, "failed", [], {"error": str(e)}, rank, attempt, clock() - t0, meta)
             out.append(rec)
             if fh:
                 fh.write(rec.to_json() + "\n")
@@ -162,11 +240,30 @@ def frequencies(lam):
     return [math.sqrt(max(x, 0.0)) / (2.0 * math.pi) for x in lam]
 
 
-def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, stream=None, **opts):
+def default_store():
+    """The initialised process group's key-value store (atomic add), or None."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return None
+    try:
+        from torch.distributed import distributed_c10d as c10d
+        return c10d._get_default_store()
+    except Exception:  # noqa: BLE001 -- no store: fall back to static LPT shares
+        return None
+
+
+_CALLS = [0]   # solve_path calls in this process (all ranks call it alike): store key prefix
+
+
+def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, stream=None, steal=True, **opts):
     """Band structure along a k-path: every rank (torch.distributed, one
     process per GPU, if initialised) solves its LPT share on its own device
-    through the C ABI and the merged, path-ordered records are returned on
-    every rank.  ``eps``: (3n,) float64 host array (P:L323-332 layout)."""
+    through the C ABI, stealing unclaimed k from slower ranks when its own
+    share is done (``steal``), and the merged, path-ordered records are
+    returned on every rank.  ``eps``: (3n,) float64 host array (P:L323-332
+    layout)."""
+    import glob
+
     import torch.distributed as dist
 
     from . import Lattice, Solver
@@ -178,12 +275,17 @@ def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, str
     lat = Lattice(a_raw, n)
     S = Solver(lat, device=device, stream=stream, **opts)
     S.set_epsilon(eps)
-    share = assign(kappas, world)[rank]
+    shares = assign(kappas, world)
+    store = default_store() if (steal and world > 1) else None
+    _CALLS[0] += 1
+    todo = StealQueue(shares, rank, store, prefix="kpath%d" % _CALLS[0]) if store is not None else shares[rank]
     ck = os.path.join(checkpoint_dir, "kpath_rank%d.jsonl" % rank) if checkpoint_dir else None
+    others = sorted(glob.glob(os.path.join(checkpoint_dir, "kpath_rank*.jsonl"))) if checkpoint_dir else []
+    meta = run_meta(nev, eps, n=tuple(n), **{k: v for k, v in opts.items()})
 
     def solve(kap):
         return S.solve(kap, nev, allow_noconv=True)
 
-    recs = run_path(solve, kappas, share, rank=rank, checkpoint=ck)
+    recs = run_path(solve, kappas, todo, rank=rank, checkpoint=ck, meta=meta, resume_from=others)
     S.close()
     return gather(recs, len(kappas))

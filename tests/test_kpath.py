@@ -116,3 +116,78 @@ def test_gather_world2_gloo_equals_single_process(tmp_path):
 def test_frequencies_convention():
     lam = [4 * np.pi ** 2, 0.0]
     assert kpath.frequencies(lam) == [1.0, 0.0]
+
+
+def test_checkpoint_ignores_other_runs(tmp_path):
+    """a checkpoint written with another nev / eps / option set
+    (meta) or another kappa for the same index is not reused."""
+    kaps = _path()[:4]
+    ck = str(tmp_path / "rank0.jsonl")
+    kpath.run_path(_fake_solve, kaps, [0, 1, 2, 3], checkpoint=ck, meta="A")
+    seen = []
+
+    def counting(kap):
+        seen.append(kap)
+        return _fake_solve(kap)
+
+    kpath.run_path(counting, kaps, [0, 1, 2, 3], checkpoint=ck, meta="B")
+    assert len(seen) == 4                                   # other meta: nothing reused
+    seen.clear()
+    moved = [kaps[0], (0.9, 0.9, 0.9), kaps[2], kaps[3]]
+    kpath.run_path(counting, moved, [0, 1, 2, 3], checkpoint=ck, meta="A")
+    assert seen == [(0.9, 0.9, 0.9)]                        # only the changed kappa re-solved
+    m1 = kpath.run_meta(16, np.ones(6), block=2)
+    assert m1 == kpath.run_meta(16, np.ones(6), block=2)
+    assert m1 != kpath.run_meta(16, np.ones(6), block=4) and m1 != kpath.run_meta(10, np.ones(6), block=2)
+
+
+def test_steal_queue_single_process_covers_all():
+    shares = kpath.assign(_path(), 3)
+    q = kpath.StealQueue(shares, 1, None)
+    got = list(q)
+    assert sorted(got) == sorted(i for s in shares for i in s)   # own share, then every other one
+    assert got[:len(shares[1])] == shares[1]
+
+
+def _steal_worker(rank, world, port, out_dir):
+    import time
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kaps = _path()
+    shares = kpath.assign(kaps, world)
+    q = kpath.StealQueue(shares, rank, kpath.default_store(), prefix="t")
+
+    def slow(kap):        # rank 0 is 20x slower per k: rank 1 must steal from it
+        time.sleep(0.2 if rank == 0 else 0.01)
+        return _fake_solve(kap)
+
+    recs = kpath.run_path(slow, kaps, q, rank=rank)
+    merged = kpath.gather(recs, len(kaps))
+    if rank == 0:
+        with open(os.path.join(out_dir, "steal.json"), "w") as f:
+            json.dump({"merged": [[r.index, r.rank, r.lam] for r in merged],
+                       "counts": [sum(1 for r in merged if r.rank == q_) for q_ in range(world)],
+                       "shares": shares}, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_work_stealing_world2_gloo():
+    """World size 2 over gloo: the slow rank's unclaimed k are taken by the
+    fast rank; every k is solved exactly once and the merged path equals a
+    single-process run."""
+    import tempfile
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_steal_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        with open(os.path.join(d, "steal.json")) as f:
+            out = json.load(f)
+    kaps = _path()
+    merged = out["merged"]
+    assert [m[0] for m in merged] == list(range(len(kaps)))
+    assert out["counts"][1] > len(out["shares"][1])            # rank 1 stole
+    single = kpath.merge([kpath.run_path(_fake_solve, kaps, range(len(kaps)))], len(kaps))
+    for m, s in zip(merged, single):
+        assert m[2] == s.lam

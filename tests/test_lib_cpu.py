@@ -145,3 +145,25 @@ def test_solver_refuses_without_gpu(bnf):
     with pytest.raises(bnf.BnfError) as e:
         bnf.Solver(L)
     assert e.value.code == bnf.ECUDA
+
+
+@pytest.mark.parametrize("idx", [1, 4, 5])
+def test_kappa_canonical_equals_oracle(bnf, idx):
+    """bnf_kappa_canonical (the ABI's raw -> canonical relabel, R10) equals the
+    oracle's kappa_from_raw on the configs whose k are given as raw kappa
+    (config 4: cyclic relabel; 5: FCC) and on a left-handed cell (sign flip)."""
+    from oracle import lattice as olat
+    from synthetic import configs
+    cfg = configs.config(idx)
+    cases = [(cfg.a_raw, cfg.n)]
+    lh = cfg.a_raw.copy()
+    lh[:, [0, 1]] = lh[:, [1, 0]]          # swap two vectors: left-handed raw triple
+    cases.append((lh, cfg.n))
+    rng = np.random.default_rng(idx)
+    for a, n in cases:
+        L = bnf.Lattice(a, n)
+        O = olat.snap(a, n)
+        assert L.perm == O.perm and L.sign3 == O.sign3
+        for _ in range(5):
+            kr = rng.uniform(-1, 1, 3)
+            assert L.kappa_from_raw(kr) == olat.kappa_from_raw(O, kr)

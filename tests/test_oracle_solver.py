@@ -105,3 +105,31 @@ def test_threaded_operator_bit_identical():
     finally:
         F._THREADS, F._WORKERS = t, w
     assert np.array_equal(z0, z1)
+
+
+@pytest.mark.parametrize("which", ["sc", "fcc", "bcc_gamma", "triclinic"])
+def test_recover_satisfies_sparse_gep(which):
+    """oracle.fftop.NFSEPOperator.recover: for an eigenpair
+    A_r y = lambda y (dense NFSEP eigh), e = B^{-1} Q_r Sigma_r y solves the
+    GEP of the independently assembled sparse Yee curl (oracle.curl,
+    geometric wrap): C^*C e = lambda B e, with e^* B e = lambda y^* y.
+    (C^*C = Q_r Sigma_r^2 Q_r^* by the SVD theorem.)"""
+    cases = {"sc": (configs.sc_vectors(), (5, 4, 6), "random:1", (0.21, -0.13, 0.4)),
+             "fcc": (configs.fcc_vectors(), (6, 6, 5), "fcc_diamond", (0.5, 0.25, 0.75)),
+             "bcc_gamma": (configs.bcc_vectors(), (6, 6, 4), "bcc_sphere_rod", (0.0, 0.0, 0.0)),
+             "triclinic": (configs.triclinic_vectors(), (6, 5, 7), "random:5", (0.2, -0.3, 0.45))}
+    a, n, shape, kap = cases[which]
+    from oracle import curl
+    L = lattice.snap(a, n)
+    eps = E.sample(shape, n, L.a, L.delta, L.a_canon)
+    op = fftop.NFSEPOperator(L, kap, eps)
+    w, Y = np.linalg.eigh(spectral.Ar_dense(L, kap, eps))
+    C = curl.curl(L, kap)
+    Bd = curl.B_diag(eps)
+    first = 2 if which == "bcc_gamma" else 0          # masked Gamma mode: 2 structural zeros (R6)
+    for i in range(first, first + 5):
+        lam, y = w[i], Y[:, i]
+        e = op.recover(y).ravel()
+        res = np.linalg.norm(C.conj().T @ (C @ e) - lam * Bd * e) / (lam * np.linalg.norm(Bd * e))
+        assert res < 1e-11, (which, i, res)
+        np.testing.assert_allclose(np.vdot(e, Bd * e).real, lam * np.vdot(y, y).real, rtol=1e-11)
