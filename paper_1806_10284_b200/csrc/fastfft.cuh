@@ -291,6 +291,103 @@ __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, doubl
     DFT<N1, S>::run(v);
 }
 
+// ------------------------------------------ warp-local variants (no CTA barrier)
+// The N2 threads of a sequence are consecutive lanes of one warp (lane =
+// w * N2 + t, W = 32 / N2 sequences per warp), so the stage exchange is an
+// N2 x N2 transpose per u inside the warp.  XSHFL = 1: by xor shuffles
+// (log2 N2 stages; element (lane t, slot u N2 + s) -> (lane s, slot u N2 + t));
+// XSHFL = 0: through a per-warp shared-memory region `xw` with __syncwarp
+// (padded layout k1 * S1 + t * S2 + w, conflict-free for 16-byte accesses).
+template <int N1, int N2>
+struct WarpXch {
+    static constexpr int W = 32 / N2;
+    static constexpr int S2 = W + 1;
+    static constexpr int S1 = N2 * S2 + 1;
+    static constexpr int size = N1 * S1;   // complex elements per warp
+};
+
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int d) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, d), __shfl_xor_sync(0xffffffffu, v.y, d));
+}
+
+template <int N1, int N2, int XSHFL>
+__device__ __forceinline__ void warp_xpose(double2 (&v)[N1], int t, int w, double2* xw) {
+    if constexpr (XSHFL) {
+#pragma unroll
+        for (int d = 1; d < N2; d <<= 1) {
+            const bool p = (t & d) != 0;
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+                for (int s = 0; s < N2; ++s) {
+                    if (s & d) continue;
+                    double2& a = v[u * N2 + s];
+                    double2& b = v[u * N2 + (s ^ d)];
+                    const double2 r = shfl_xor2(p ? a : b, d);
+                    if (p) a = r;
+                    else b = r;
+                }
+        }
+    } else {
+        using X = WarpXch<N1, N2>;
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) xw[k1 * X::S1 + t * X::S2 + w] = v[k1];
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int tt = 0; tt < N2; ++tt) v[u * N2 + tt] = xw[(t + N2 * u) * X::S1 + tt * X::S2 + w];
+        __syncwarp();
+    }
+}
+
+// As fft_fwd (natural -> stage-2 layout), warp-local.  `root` as in fft_fwd
+// (global [k1][t] table, or a shared-memory copy).
+template <int N1, int N2, int S, int XSHFL>
+__device__ __forceinline__ void fft_fwd_w(double2 (&v)[N1], int t, int w, double2* xw, const double2* root) {
+    DFT<N1, S>::run(v);
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) {
+            const double2 r = root[k1 * N2 + t];
+            v[k1] = cmul(v[k1], S > 0 ? r : cconj(r));
+        }
+    }
+    warp_xpose<N1, N2, XSHFL>(v, t, w, xw);
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u) {
+        double2 a[N2];
+#pragma unroll
+        for (int q = 0; q < N2; ++q) a[q] = v[u * N2 + q];
+        DFT<N2, S>::run(a);
+#pragma unroll
+        for (int q = 0; q < N2; ++q) v[u * N2 + q] = a[q];
+    }
+}
+
+// As fft_mirror (stage-2 -> natural layout), warp-local.
+template <int N1, int N2, int S, int XSHFL>
+__device__ __forceinline__ void fft_mirror_w(double2 (&v)[N1], int t, int w, double2* xw, const double2* root) {
+#pragma unroll
+    for (int u = 0; u < N1 / N2; ++u) {
+        double2 a[N2];
+#pragma unroll
+        for (int q = 0; q < N2; ++q) a[q] = v[u * N2 + q];
+        DFT<N2, S>::run(a);
+#pragma unroll
+        for (int q = 0; q < N2; ++q) v[u * N2 + q] = a[q];
+    }
+    warp_xpose<N1, N2, XSHFL>(v, t, w, xw);
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) {
+            const double2 r = root[k1 * N2 + t];
+            v[k1] = cmul(v[k1], S > 0 ? r : cconj(r));
+        }
+    }
+    DFT<N1, S>::run(v);
+}
+
 // ------------------------------------------- twiddle sequences (no long chains)
 // w^b for the N1 elements a thread holds after fft_fwd (stage-2 layout,
 // b = t + N2 u + N1 k2) or before it (natural layout, b = N2 m + t), built from

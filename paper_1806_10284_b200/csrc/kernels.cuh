@@ -57,6 +57,7 @@ struct OpArgs {
     unsigned long long* prof;   // optional per-phase cycle counters (plane pass), or null
     int plane_hint;             // L2 plane: evict-last / evict-first store hints (1)
     int plane_l2;               // plane pass: one CTA per plane, strips exchanged through L2 (1) or cluster/DSMEM (0)
+    int plane_w;                // plane pass with warp-local FFT exchanges: 0 off, 1 shared memory, 2 shuffles
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -107,6 +108,7 @@ size_t cg_partials_per_vec(const OpArgs& a);
 // x-DFT*, twiddle*, y-DFT* on every (component, z-plane) of nslab = 3*nvec
 // component slabs, one HBM read + write.  Square xy planes with a fast plan.
 bool plane_supported(const OpArgs& a);
+bool plane_w_supported(const OpArgs& a);
 
 // Persistent, cp.async-pipelined z passes (zpass.cu).  cg == nullptr: plain
 // op (0 = A_r, 1 = M); otherwise the CG-fused variants (x update deferred:

@@ -397,6 +397,159 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-local variant ("plane_w"): one CTA per (component, z-plane)
+// as k_plane_l2, strips exchanged through L2, but every FFT sequence lives in
+// N2 consecutive lanes of ONE warp (lane = w N2 + t, W = 32 / N2 sequences per
+// warp), so the FFT stage exchange is warp-local -- xor shuffles (XSHFL = 1) or
+// a padded per-warp shared-memory region with __syncwarp (XSHFL = 0) -- and the
+// warps of a CTA run their strips independently: the only CTA barriers are the
+// two phase boundaries (Y -> X -> Y*).  Stage-twiddle tables and the plane's
+// B^{-1} material indices sit in shared memory.
+template <int N1, int N2, int NWARP, int XSHFL>
+struct PlaneWCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int W = 32 / N2;               // sequences per warp
+    static constexpr int CW = W * NWARP;            // sequences per strip pass
+    static constexpr int P = N / CW;                // strip passes per phase
+    static constexpr int NT = 32 * NWARP;
+    static constexpr int XS = XSHFL ? 0 : fast::WarpXch<N1, N2>::size;   // complex per warp
+    static constexpr size_t smem = (size_t)(NWARP * XS + 2 * N) * sizeof(double2) + (size_t)N * N + 256 * sizeof(double);
+};
+
+template <int N1, int N2, int NWARP, int CG, int XSHFL>
+__global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
+    using C = PlaneWCfg<N1, N2, NWARP, XSHFL>;
+    constexpr int N = C::N, W = C::W, CW = C::CW, P = C::P, NT = C::NT;
+    static_assert(N % CW == 0 && 32 % N2 == 0 && N1 % N2 == 0, "plane_w plan");
+    extern __shared__ double2 D[];
+    const ModeP& p = a.mp;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int w = lane / N2, t = lane % N2;
+    const int c = blockIdx.x;
+    const int vl = blockIdx.y + a.comp0;
+    const int l = vl % 3;
+    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    double2* xw = D + warp * C::XS;                         // this warp's exchange region
+    double2* ry = D + NWARP * C::XS;                        // y stage twiddles [k1][t]
+    double2* rx = ry + N;                                   // x stage twiddles
+    unsigned char* eps_s = reinterpret_cast<unsigned char*>(rx + N);   // [N][N] material indices
+    double* lut_s = reinterpret_cast<double*>(eps_s + N * N);
+    const bool epf = a.eps_idx != nullptr;
+    for (int q = tid; q < N; q += NT) {
+        ry[q] = __ldg(a.py.root2 + q);
+        rx[q] = __ldg(a.px.root2 + q);
+    }
+    if (epf) {
+        for (int q = tid; q < 256; q += NT) lut_s[q] = __ldg(a.eps_lut + q);
+        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c;
+        for (int q = tid; q < N * N / 16; q += NT) cp_async16(eps_s + 16 * q, src + 16 * q);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    __syncthreads();   // stage-twiddle tables
+    const unsigned n12 = (unsigned)p.n12;
+    const unsigned long long s3 = (unsigned long long)p.n3;
+    const unsigned long long pol_keep = a.plane_hint ? l2_policy_last() : 0ull;
+    const unsigned long long pol_out = a.plane_hint ? l2_policy_first() : 0ull;
+    double2 v[N1];
+    // ---------------- phase Y: y-DFT (+) of columns i, twiddle e^{-2 pi i b m1 i / n12} ----------------
+#pragma unroll 1
+    for (int r = 0; r < P; ++r) {
+        const int i = r * CW + warp * W + w;
+        const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        fast::fft_fwd_w<N1, N2, 1, XSHFL>(v, t, w, xw, ry);
+        const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
+        const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
+        const double2 wk = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3));
+        fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_keep);
+                else *dst = v[u * N2 + k2];
+            }
+    }
+    if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();   // every column strip is written (block-scope visibility) before rows are read
+    // ---------------- phase X: x-DFT (+), 1/(n eps) [+ (p, Mp)], x-DFT (-) of rows b ----------------
+    double pmp = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < P; ++r) {
+        const int b = r * CW + warp * W + w;
+        double2* row = plane + (size_t)b * N;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + t];
+        fast::fft_fwd_w<N1, N2, 1, XSHFL>(v, t, w, xw, rx);
+        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+        auto scale = [&](auto eps_at) {
+#pragma unroll
+            for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) {
+                    const int aa = t + N2 * u + N1 * k2;
+                    const double s_ = a.inv_n * eps_at(aa);
+                    const double2 x = v[u * N2 + k2];
+                    if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);   // (p, M p) = sum |T v|^2 / (n eps)
+                    v[u * N2 + k2] = cscale(x, s_);
+                }
+        };
+        if (epf) scale([&](int aa) { return lut_s[eps_s[b * N + aa]]; });
+        else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
+        fast::fft_mirror_w<N1, N2, -1, XSHFL>(v, t, w, xw, rx);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+            if (a.plane_hint) st_hint(row + N2 * m + t, v[m], pol_keep);
+            else row[N2 * m + t] = v[m];
+        }
+    }
+    __syncthreads();
+    // ---------------- phase Y*: conj twiddle, y-DFT (-) of columns ----------------
+#pragma unroll 1
+    for (int r = 0; r < P; ++r) {
+        const int i = r * CW + warp * W + w;
+        const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
+        const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
+        fast::twiddle_natural<N1, N2>(v, wt, wu);
+        fast::fft_fwd_w<N1, N2, -1, XSHFL>(v, t, w, xw, ry);
+#pragma unroll
+        for (int u = 0; u < N1 / N2; ++u)
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_out);
+                else *dst = v[u * N2 + k2];
+            }
+    }
+    if (CG) {
+        const int vec = vl / 3;
+        const int nb = gridDim.x * 3;
+        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        const long long lin = (long long)vl * gridDim.x + blockIdx.x;
+        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
+    }
+}
+
+template <int N1, int N2, int NWARP, int XSHFL>
+cudaError_t launch_plane_w_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    using C = PlaneWCfg<N1, N2, NWARP, XSHFL>;
+    const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
+    auto run = [&](auto kern, auto cgarg) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+        if (e != cudaSuccess) return e;
+        kern<<<g, C::NT, C::smem, st>>>(U, a, cgarg);
+        return cudaGetLastError();
+    };
+    if (cg) return run(k_plane_w<N1, N2, NWARP, 1, XSHFL>, *cg);
+    return run(k_plane_w<N1, N2, NWARP, 0, XSHFL>, CGFuse{});
+}
+
 template <int N1, int N2, int P>
 cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
@@ -460,7 +613,20 @@ bool plane_supported(const OpArgs& a) {
     }
 }
 
+bool plane_w_supported(const OpArgs& a) {
+    return a.fast && a.mp.n1 == a.mp.n2 && (a.mp.n1 == 64 || a.mp.n1 == 128 || a.mp.n1 == 256);
+}
+
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    if (a.plane_w && plane_w_supported(a)) {   // warp-local FFT exchanges (1: smem, 2: shuffles)
+        const bool sh = a.plane_w == 2;
+        switch (a.mp.n1) {
+            case 64: return sh ? launch_plane_w_t<8, 8, 8, 1>(a, U, nslab, cg, st) : launch_plane_w_t<8, 8, 8, 0>(a, U, nslab, cg, st);
+            case 128: return sh ? launch_plane_w_t<16, 8, 8, 1>(a, U, nslab, cg, st) : launch_plane_w_t<16, 8, 8, 0>(a, U, nslab, cg, st);
+            case 256: return sh ? launch_plane_w_t<16, 16, 8, 1>(a, U, nslab, cg, st) : launch_plane_w_t<16, 16, 8, 0>(a, U, nslab, cg, st);
+            default: break;
+        }
+    }
     if (a.plane_l2) {   // one CTA per plane, strips exchanged through L2
         switch (a.mp.n1) {
             case 64: return launch_plane_l2_t<8, 8, 2>(a, U, nslab, cg, st);

@@ -422,7 +422,8 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     if (s->use_z2) RUN("zfwd2", launch_zfwd2(s->args, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
-        RUN(s->args.plane_l2 ? "plane_l2" : "plane", launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+        RUN(s->args.plane_w ? (s->args.plane_w == 2 ? "plane_ws" : "plane_w") : s->args.plane_l2 ? "plane_l2" : "plane",
+            launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
     } else {
         RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
@@ -440,8 +441,12 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
 int autotune_plane(bnf_solver* s, int nvec) {
     if (s->plane_tuned || !s->plane_ok) return BNF_OK;
     s->plane_tuned = true;
-    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE")) {
+    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE") || std::getenv("BNF_PLANE_W")) {
         s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? std::atoi(std::getenv("BNF_PLANE_L2")) : 0;
+        s->args.plane_w = std::getenv("BNF_PLANE_W") ? std::atoi(std::getenv("BNF_PLANE_W")) : 0;
+        if (std::getenv("BNF_NO_PLANE")) s->args.plane_w = 0;
+        s->use_plane = std::getenv("BNF_NO_PLANE") == nullptr;
+        s->kver++;
         return BNF_OK;
     }
     const long long N = 2 * s->n;
@@ -453,14 +458,20 @@ int autotune_plane(bnf_solver* s, int nvec) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2
-    float best[3] = {0.f, 0.f, 0.f};
+    // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2,
+    // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles)
+    const int nvar = plane_w_supported(s->args) ? 5 : 3;
+    float best[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;
-    for (int variant = 0; variant < 3; ++variant) {
+    auto set = [&](int variant) {
         s->use_plane = variant >= 1;
         s->args.plane_l2 = variant == 2 ? 1 : 0;
+        s->args.plane_w = variant >= 3 ? variant - 2 : 0;
+    };
+    for (int variant = 0; variant < nvar; ++variant) {
+        set(variant);
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
         CK(cudaEventRecord(e0, s->st));
         for (int r = 0; r < 3; ++r) TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));
@@ -469,10 +480,9 @@ int autotune_plane(bnf_solver* s, int nvec) {
         CK(cudaEventElapsedTime(&best[variant], e0, e1));
     }
     int pick = 0;
-    for (int variant = 1; variant < 3; ++variant)
+    for (int variant = 1; variant < nvar; ++variant)
         if (best[variant] < best[pick]) pick = variant;
-    s->use_plane = pick >= 1;
-    s->args.plane_l2 = pick == 2 ? 1 : 0;
+    set(pick);
     s->matvecs = mv0;
     s->prof.on = prof;
     cudaEventDestroy(e0);
@@ -677,7 +687,9 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
-                RUN(s->args.plane_l2 ? "plane_l2_cg" : "plane_cg", launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+                RUN(s->args.plane_w ? (s->args.plane_w == 2 ? "plane_ws_cg" : "plane_w_cg")
+                                    : s->args.plane_l2 ? "plane_l2_cg" : "plane_cg",
+                    launch_plane(s->args, U, 3 * nvec, &cg, s->st));
                 RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
@@ -1325,6 +1337,26 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     // small device scratch: gram_host / gemm_nn_host stage p x 8 blocks at offset 64
     CK(s->small.ensure((size_t)(64 + 8 * std::max<long long>((long long)(maxsteps + 1) * b, want)) * sizeof(double2)));
     double2* V = s->V.as<double2>();
+    // start block: seeded counter-based normals, Gamma mode masked (R6)
+    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st));
+    if (s->o.warm && s->prev_want > 0) {
+        // Warm start (DESIGN R17): start block = fixed pseudo-random combinations of
+        // the previous solve's Ritz vectors (neighbouring k on the path) plus 1e-3 of
+        // the random block; Gamma mode masked.  Only the start block changes; the
+        // iteration, its tolerance and the returned eigenpairs are as before.
+        const int pw = s->prev_want;
+        std::vector<cd> Wm((size_t)pw * b);
+        unsigned long long h = 0x9E3779B97F4A7C15ull;
+        for (auto& x : Wm) {
+            h ^= h >> 33;
+            h *= 0xff51afd7ed558ccdull;
+            h ^= h >> 33;
+            x = cd(((double)(h >> 11) / 9007199254740992.0) - 0.5, 0.0);
+        }
+        TRY(gemm_nn_host(s, s->Yv.as<double2>(), pw, Wm, b, V, 1.0, 1e-3));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st));
+    }
     bool ok = true;
     std::vector<cd> R0;
     TRY(chol_qr2(s, V, b, R0, ok));
