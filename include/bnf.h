@@ -149,6 +149,13 @@ typedef struct {
                                    Rayleigh-Ritz while max ||A_r y - lambda y|| / ||y|| > res_tol
                                    (north-star eigenvector bar 1e-8; DESIGN R19) */
     int max_polish;             /* at most this many such extra steps (3) */
+    int slabs;                  /* 1 (default): whole grid.  P > 1: run the slab-decomposed operator of
+                                   SURVEY §8(e) on this one device ("virtual slabs", the multi-GPU data
+                                   layout with the all-to-alls as device copies): Fourier-side vectors
+                                   are laid out [slab][half][k][jl][i] with jl < n2/P (slab r holds
+                                   j = r n2/P + jl), real-space work in z-slabs of n3/P planes.
+                                   Needs n2, n3 divisible by P, a square xy plane of 64/128/256.
+                                   bnf_apply_Ar / BNF_VEC_Y use that layout; BNF_VEC_E is refused. */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);

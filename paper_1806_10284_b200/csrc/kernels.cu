@@ -478,17 +478,30 @@ __global__ void k_bloch(double2* __restrict__ U, long long n, int n1, int n2, in
     }
 }
 
-__global__ void k_sigma_table(ModeP p, double* __restrict__ sigma) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < p.n;
+// sigma = Lambda_q^{1/2} over `count` Fourier entries laid out as consecutive
+// j-slabs [slab][k][jl][i] of n2loc rows each, starting at row j0 (one slab
+// covering all j: the plain [k][j][i] layout)
+__global__ void k_sigma_table(ModeP p, double* __restrict__ sigma, int j0, int n2loc, long long count) {
+    const long long nloc = (long long)p.n1 * n2loc * p.n3;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
          t += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(t % p.n1);
-        const int j = (int)((t / p.n1) % p.n2);
-        const int k = (int)(t / p.n12);
+        const long long r = t / nloc, loc = t - r * nloc;
+        const int i = (int)(loc % p.n1);
+        const int j = j0 + (int)(r * n2loc + (loc / p.n1) % n2loc);
+        const int k = (int)(loc / ((long long)p.n1 * n2loc));
         double2 lam[3];
         mode_lambdas(p, i, j, k, lam);
         const double q = cabs2(lam[0]) + cabs2(lam[1]) + cabs2(lam[2]);
-        sigma[t] = (t == p.gamma) ? 0.0 : sqrt(q);
+        const long long flat = (long long)i + (long long)p.n1 * (j + (long long)p.n2 * k);
+        sigma[t] = (flat == p.gamma) ? 0.0 : sqrt(q);
     }
+}
+
+// index of the sigma entry of element t of a batch of vectors of 2 nh entries
+// laid out [slab][half][local] (slabs of 2 nloc; one slab: [half][local])
+__device__ __forceinline__ long long sig_index(long long t, long long nh, long long nloc) {
+    const long long u = t % (2 * nh);
+    return (u / (2 * nloc)) * nloc + u % nloc;
 }
 
 // ---------------------------------------------------------- BLAS-1 / tall-skinny
@@ -606,10 +619,10 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double2* X, int p, const 
 
 // Y = X * sigma^{+-1} on both halves of every 2n vector (masked: 0)
 __global__ void k_scale_sigma(const double2* __restrict__ X, double2* __restrict__ Y, const double* __restrict__ sigma,
-                              long long n, long long total, int inverse) {
+                              long long n, long long nloc, long long total, int inverse) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
-        const double s = sigma[t % n];
+        const double s = sigma[sig_index(t, n, nloc)];
         const double f = inverse ? (s > 0.0 ? 1.0 / s : 0.0) : s;
         Y[t] = cscale(X[t], f);
     }
@@ -624,7 +637,7 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
 
 // Counter-based normal deviates (Box-Muller on two hashed uniforms).
 __global__ void k_fill_random(double2* __restrict__ X, long long total, unsigned long long seed, long long offset,
-                              const double* __restrict__ sigma, long long n) {
+                              const double* __restrict__ sigma, long long n, long long nloc) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const unsigned long long h1 = splitmix64(seed ^ splitmix64((unsigned long long)(t + offset) * 2ull));
@@ -634,7 +647,7 @@ __global__ void k_fill_random(double2* __restrict__ X, long long total, unsigned
         const double rad = sqrt(-2.0 * log(u1));
         double s, c;
         sincospi(2.0 * u2, &s, &c);
-        const double m = (sigma != nullptr && sigma[t % n] == 0.0) ? 0.0 : 1.0;
+        const double m = (sigma != nullptr && sigma[sig_index(t, n, nloc)] == 0.0) ? 0.0 : 1.0;
         X[t] = make_double2(m * rad * c, m * rad * s);
     }
 }
@@ -1252,8 +1265,10 @@ cudaError_t launch_bloch_phase(const OpArgs& a, double2* U, int nvec, double kap
     return cudaGetLastError();
 }
 
-cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st) {
-    k_sigma_table<<<grid_for(mp.n, 256), 256, 0, st>>>(mp, sigma);
+cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st, int j0, int n2loc, long long count) {
+    if (n2loc <= 0) n2loc = mp.n2;
+    if (count <= 0) count = mp.n;
+    k_sigma_table<<<grid_for(count, 256), 256, 0, st>>>(mp, sigma, j0, n2loc, count);
     return cudaGetLastError();
 }
 
@@ -1308,16 +1323,16 @@ cudaError_t launch_gemm_nn(const double2* X, int p, const double2* H, int q, dou
 }
 
 cudaError_t launch_scale_sigma(const double2* X, double2* Y, const double* sigma, long long n, int nvec, int inverse,
-                               cudaStream_t st) {
+                               cudaStream_t st, long long nloc) {
     const long long total = (long long)2 * n * nvec;
-    k_scale_sigma<<<grid_for(total, 256), 256, 0, st>>>(X, Y, sigma, n, total, inverse);
+    k_scale_sigma<<<grid_for(total, 256), 256, 0, st>>>(X, Y, sigma, n, nloc > 0 ? nloc : n, total, inverse);
     return cudaGetLastError();
 }
 
 cudaError_t launch_fill_random(double2* X, long long N, int nvec, unsigned long long seed, long long offset,
-                               const double* sigma, long long n, cudaStream_t st) {
+                               const double* sigma, long long n, cudaStream_t st, long long nloc) {
     const long long total = N * nvec;
-    k_fill_random<<<grid_for(total, 256), 256, 0, st>>>(X, total, seed, offset, sigma, n);
+    k_fill_random<<<grid_for(total, 256), 256, 0, st>>>(X, total, seed, offset, sigma, n, nloc > 0 ? nloc : n);
     return cudaGetLastError();
 }
 

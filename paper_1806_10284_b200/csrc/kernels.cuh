@@ -58,6 +58,14 @@ struct OpArgs {
     int plane_hint;             // L2 plane: evict-last / evict-first store hints (1)
     int plane_l2;               // plane pass: one CTA per plane, strips exchanged through L2 (1) or cluster/DSMEM (0)
     int plane_w;                // plane pass with warp-local FFT exchanges: 0 off, 1 shared memory, 2 shuffles
+    // Slab decomposition: this launch works on slab `slab` of `nslab`.
+    // Fourier-side arrays hold the j-slab [j0, j0 + n2loc) (all i, k): [vec][half][k][jl][i];
+    // real-space arrays hold the z-slab of n3loc planes (all a, b): [vec][l][cl][b][a].
+    // nloc = elements per component per vector on the slab (n / nslab).  nslab = 1: whole grid.
+    int j0, n2loc, n3loc, slab, nslab;
+    long long nloc;
+    long long vsf;              // Fourier-side vector stride (elements): 2 nloc, or 2n for virtual slabs
+    long long nblk;             // n1 n2loc n3loc: one (slab pair, vector, component) exchange block
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -125,7 +133,8 @@ cudaError_t launch_cg_finish(const CGFuse& cg, int which, int nvec, cudaStream_t
 cudaError_t launch_cg_xfinal(double2* X, const double2* P, const double* alpha, long long N, int nvec, cudaStream_t st);
 cudaError_t launch_plane(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st);
 
-cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st);
+cudaError_t launch_sigma_table(const ModeP& mp, double* sigma, cudaStream_t st, int j0 = 0, int n2loc = 0,
+                               long long count = 0);
 
 // vectors of length N (complex), nvec of them, stored back to back
 cudaError_t launch_dot_partial(const double2* X, const double2* Y, long long N, int nvec, double2* partial,
@@ -137,9 +146,9 @@ cudaError_t launch_gemm_tn_final(const double2* partial, int nblk, int pq, doubl
 cudaError_t launch_gemm_nn(const double2* X, int p, const double2* H, int q, double2* Y, long long N,
                            double alpha, double beta, cudaStream_t st);
 cudaError_t launch_scale_sigma(const double2* X, double2* Y, const double* sigma, long long n, int nvec,
-                               int inverse, cudaStream_t st);
+                               int inverse, cudaStream_t st, long long nloc = 0);
 cudaError_t launch_fill_random(double2* X, long long N, int nvec, unsigned long long seed, long long offset,
-                               const double* sigma, long long n, cudaStream_t st);
+                               const double* sigma, long long n, cudaStream_t st, long long nloc = 0);
 cudaError_t launch_copy(double2* dst, const double2* src, long long count, cudaStream_t st);
 
 // CG (batched over nvec right-hand sides)

@@ -137,16 +137,16 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     // clusters loop over the planes (component slab, z-plane); the launch uses one
     // cluster per plane (a persistent grid measured slower on B200)
     const int ncl = gridDim.x / P, cid = blockIdx.x / P;
-    const int total = p.n3 * nslab;
+    const int total = a.n3loc * nslab;
     for (int pl = cid; pl < total; pl += ncl) {
-    const int c = pl % p.n3;
-    const int vl = pl / p.n3 + a.comp0;
+    const int c = pl % a.n3loc;
+    const int vl = pl / a.n3loc + a.comp0;
     const int l = vl % 3;
-    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    double2* plane = U + (size_t)vl * a.nloc + (size_t)c * N * N;
     double2 v[N1];
     // B^{-1} material indices of this CTA's phase-X rows (contiguous CW*N bytes), prefetched
     if (epf) {
-        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * ((size_t)r * CW + (size_t)N * c);
+        const unsigned char* src = a.eps_idx + (size_t)l * a.nloc + (size_t)N * ((size_t)r * CW + (size_t)N * c);
         for (int q = threadIdx.x; q < CW * N / 16; q += C::NT) cp_async16(eps_s + 16 * q, src + 16 * q);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     BNF_PROBE(5);   // x-FFT
     double pmp = 0.0;
     {
-        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+        const size_t rowofs = (size_t)l * a.nloc + (size_t)N * ((size_t)b + (size_t)N * c);
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         // per-CTA partials of (p, M p) for every vector
         const int nvec = nslab / 3;
         const int nb = gridDim.x;
-        if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
+        if (tid < nvec) cgf.part_x[((size_t)tid * a.nslab + a.slab) * nb + blockIdx.x] = acc_s[tid];
         __syncthreads();
-        if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;   // alpha: k_cg_finish after this pass
+        if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb * a.nslab;   // alpha: k_cg_finish after this pass
     }
 }
 
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 // memory: the plane (N*N*16 B, 256 KB at 128^2) is re-read while it is hot
 // in L2, so DRAM still sees one read and one write per element, and there
 // are no cluster barriers or DSMEM stores.  Two CTAs per SM overlap.
-template <int N1, int N2, int P, int CG>
+template <int N1, int N2, int P, int CG, int SL = 0>
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
@@ -287,14 +287,20 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const int c = blockIdx.x;
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
-    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    // plane rows b: one slab -> plane + b N; virtual / distributed slabs -> the block of the
+    // source slab b / n2loc, row b % n2loc ([r][vec][l][cl][jl][a], blocks of nblk)
+    double2* plane = U + (size_t)vl * (SL ? a.nblk : p.n) + (size_t)c * (SL ? a.n2loc : N) * N;
+    auto rowp = [&](int b) -> double2* {
+        if constexpr (SL == 0) return plane + (size_t)b * N;
+        else return plane + (size_t)(b / a.n2loc) * ((size_t)(gridDim.y / 3) * 3 * a.nblk) + (size_t)(b % a.n2loc) * N;
+    };
     constexpr bool EPF = (N % 16) == 0 && N <= 128;   // whole-plane index prefetch fits next to D
     unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);   // [N][N] material indices
     double* lut_s = reinterpret_cast<double*>(eps_s + (EPF ? N * N : 0));
     const bool epf = EPF && a.eps_idx != nullptr;
     if (epf) {
         for (int q = tid; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
-        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c;
+        const unsigned char* src = a.eps_idx + (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * N * c;
         for (int q = tid; q < N * N / 16; q += C::NT) cp_async16(eps_s + 16 * q, src + 16 * q);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
         fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
         const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
         const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
@@ -320,12 +326,12 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) st_hint(plane + (size_t)(t + N2 * u + N1 * k2) * N + i, v[u * N2 + k2], pol_keep);
+                for (int k2 = 0; k2 < N2; ++k2) st_hint(rowp(t + N2 * u + N1 * k2) + i, v[u * N2 + k2], pol_keep);
         } else {
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+                for (int k2 = 0; k2 < N2; ++k2) rowp(t + N2 * u + N1 * k2)[i] = v[u * N2 + k2];
         }
     }
     if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -334,11 +340,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     double pmp = 0.0;
     for (int r = 0; r < P; ++r) {
         const int b = r * CW + rw;
-        double2* row = plane + (size_t)b * N;
+        double2* row = rowp(b);
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + tx];
         fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
-        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+        const size_t rowofs = (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * ((size_t)b + (size_t)N * c);
         // 1/(n eps) scaling (+ CG partial); the ε source is chosen once per strip, not per element
         auto scale = [&](auto eps_at) {
 #pragma unroll
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
         const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
         const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
         fast::twiddle_natural<N1, N2>(v, wt, wu);
@@ -379,21 +385,21 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) st_hint(plane + (size_t)(t + N2 * u + N1 * k2) * N + i, v[u * N2 + k2], pol_out);
+                for (int k2 = 0; k2 < N2; ++k2) st_hint(rowp(t + N2 * u + N1 * k2) + i, v[u * N2 + k2], pol_out);
         } else {
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) plane[(size_t)(t + N2 * u + N1 * k2) * N + i] = v[u * N2 + k2];
+                for (int k2 = 0; k2 < N2; ++k2) rowp(t + N2 * u + N1 * k2)[i] = v[u * N2 + k2];
         }
     }
     if (CG) {
         // this plane's (p, M p) partial; alpha is formed by k_cg_finish after this pass
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        cg_block_partial(pmp, cgf.part_x + ((size_t)vec * (SL ? a.nslab : 1) + (SL ? a.slab : 0)) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
+        if (lin == 0 && tid == 0) *cgf.nb_x = SL ? nb * a.nslab : nb;
     }
 }
 
@@ -417,7 +423,7 @@ struct PlaneWCfg {
     static constexpr size_t smem = (size_t)(NWARP * XS + 2 * N) * sizeof(double2) + (size_t)N * N + 256 * sizeof(double);
 };
 
-template <int N1, int N2, int NWARP, int CG, int XSHFL>
+template <int N1, int N2, int NWARP, int CG, int XSHFL, int SL = 0>
 __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneWCfg<N1, N2, NWARP, XSHFL>;
     constexpr int N = C::N, W = C::W, CW = C::CW, P = C::P, NT = C::NT;
@@ -429,7 +435,13 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
     const int c = blockIdx.x;
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
-    double2* plane = U + (size_t)vl * p.n + (size_t)c * N * N;
+    // plane rows b: one slab -> plane + b N; virtual / distributed slabs -> the block of the
+    // source slab b / n2loc, row b % n2loc ([r][vec][l][cl][jl][a], blocks of nblk)
+    double2* plane = U + (size_t)vl * (SL ? a.nblk : p.n) + (size_t)c * (SL ? a.n2loc : N) * N;
+    auto rowp = [&](int b) -> double2* {
+        if constexpr (SL == 0) return plane + (size_t)b * N;
+        else return plane + (size_t)(b / a.n2loc) * ((size_t)(gridDim.y / 3) * 3 * a.nblk) + (size_t)(b % a.n2loc) * N;
+    };
     double2* xw = D + warp * C::XS;                         // this warp's exchange region
     double2* ry = D + NWARP * C::XS;                        // y stage twiddles [k1][t]
     double2* rx = ry + N;                                   // x stage twiddles
@@ -442,7 +454,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
     }
     if (epf) {
         for (int q = tid; q < 256; q += NT) lut_s[q] = __ldg(a.eps_lut + q);
-        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c;
+        const unsigned char* src = a.eps_idx + (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * N * c;
         for (int q = tid; q < N * N / 16; q += NT) cp_async16(eps_s + 16 * q, src + 16 * q);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
         const int i = r * CW + warp * W + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
         fast::fft_fwd_w<N1, N2, 1, XSHFL>(v, t, w, xw, ry);
         const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
         const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
@@ -468,7 +480,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
-                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                double2* dst = rowp(t + N2 * u + N1 * k2) + i;
                 if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_keep);
                 else *dst = v[u * N2 + k2];
             }
@@ -480,11 +492,11 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
 #pragma unroll 1
     for (int r = 0; r < P; ++r) {
         const int b = r * CW + warp * W + w;
-        double2* row = plane + (size_t)b * N;
+        double2* row = rowp(b);
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + t];
         fast::fft_fwd_w<N1, N2, 1, XSHFL>(v, t, w, xw, rx);
-        const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)b + (size_t)N * c);
+        const size_t rowofs = (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * ((size_t)b + (size_t)N * c);
         auto scale = [&](auto eps_at) {
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
@@ -513,7 +525,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
         const int i = r * CW + warp * W + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = plane[(size_t)(N2 * m + t) * N + i];
+        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
         const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
         const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
         fast::twiddle_natural<N1, N2>(v, wt, wu);
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
-                double2* dst = plane + (size_t)(t + N2 * u + N1 * k2) * N + i;
+                double2* dst = rowp(t + N2 * u + N1 * k2) + i;
                 if (a.plane_hint) st_hint(dst, v[u * N2 + k2], pol_out);
                 else *dst = v[u * N2 + k2];
             }
@@ -530,22 +542,26 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
     if (CG) {
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        cg_block_partial(pmp, cgf.part_x + (size_t)vec * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        cg_block_partial(pmp, cgf.part_x + ((size_t)vec * (SL ? a.nslab : 1) + (SL ? a.slab : 0)) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
+        if (lin == 0 && tid == 0) *cgf.nb_x = SL ? nb * a.nslab : nb;
     }
 }
 
 template <int N1, int N2, int NWARP, int XSHFL>
 cudaError_t launch_plane_w_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneWCfg<N1, N2, NWARP, XSHFL>;
-    const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
+    const dim3 g((unsigned)a.n3loc, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
         if (e != cudaSuccess) return e;
         kern<<<g, C::NT, C::smem, st>>>(U, a, cgarg);
         return cudaGetLastError();
     };
+    if (a.nslab > 1) {
+        if (cg) return run(k_plane_w<N1, N2, NWARP, 1, XSHFL, 1>, *cg);
+        return run(k_plane_w<N1, N2, NWARP, 0, XSHFL, 1>, CGFuse{});
+    }
     if (cg) return run(k_plane_w<N1, N2, NWARP, 1, XSHFL>, *cg);
     return run(k_plane_w<N1, N2, NWARP, 0, XSHFL>, CGFuse{});
 }
@@ -555,13 +571,17 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
     using C = PlaneCfg<N1, N2, P>;
     constexpr bool EPF = (C::N % 16) == 0 && C::N <= 128;
     const size_t smem = (size_t)C::SMEM * sizeof(double2) + (EPF ? (size_t)C::N * C::N : 0) + 256 * sizeof(double);
-    const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
+    const dim3 g((unsigned)a.n3loc, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<g, C::NT, smem, st>>>(U, a, cgarg);
         return cudaGetLastError();
     };
+    if (a.nslab > 1) {
+        if (cg) return run(k_plane_l2<N1, N2, P, 1, 1>, *cg);
+        return run(k_plane_l2<N1, N2, P, 0, 1>, CGFuse{});
+    }
     if (cg) return run(k_plane_l2<N1, N2, P, 1>, *cg);
     return run(k_plane_l2<N1, N2, P, 0>, CGFuse{});
 }
@@ -581,7 +601,7 @@ cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse*
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const int total = a.mp.n3 * nslab;
+    const int total = a.n3loc * nslab;
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

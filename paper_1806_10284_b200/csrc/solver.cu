@@ -350,6 +350,8 @@ struct bnf_solver {
     double2* h_small = nullptr;  // pinned scratch for small matrices
     size_t h_small_cap = 0;
     int nblk = 592;
+    int nsl = 1;              // virtual slabs on this device (opts.slabs)
+    DevBuf Ub;                // plane-side buffer of the slab exchange (3n per vector)
     Profiler prof;
     long long matvecs = 0;
     long long inner_iters = 0;
@@ -412,18 +414,78 @@ int ensure_small_host(bnf_solver* s, size_t count) {
 // ------------------------------------------------------------- operator
 int ensure_work(bnf_solver* s, int nvec) {
     CK(s->U.ensure((size_t)3 * s->n * nvec * sizeof(double2)));
+    if (s->nsl > 1) CK(s->Ub.ensure((size_t)3 * s->n * nvec * sizeof(double2)));
     return BNF_OK;
+}
+
+// ---------------------------------------------------------- virtual slabs
+// OpArgs of slab r of the slab decomposition: Fourier side =
+// j-slab [r n2/P, (r+1) n2/P) of every vector, real side = z-slab of n3/P
+// planes; vectors stay contiguous 2n arrays laid out [slab][half][k][jl][i]
+// (Lanczos / CG BLAS are layout-agnostic), eps in [slab][l][cl][b][a].
+OpArgs slab_args(const bnf_solver* s, int r) {
+    OpArgs a = s->args;
+    if (s->nsl == 1) return a;
+    const int P = s->nsl;
+    a.slab = r;
+    a.nslab = P;
+    a.n2loc = s->L.n[1] / P;
+    a.n3loc = s->L.n[2] / P;
+    a.j0 = r * a.n2loc;
+    a.nloc = s->n / P;
+    a.nblk = a.nloc / P;
+    a.vsf = 2 * s->n;
+    if (a.eps_idx) a.eps_idx += (size_t)r * 3 * a.nloc;
+    if (a.eps_inv) a.eps_inv += (size_t)r * 3 * a.nloc;
+    return a;
+}
+
+// The all-to-all of the slab decomposition as device copies: plane-side slab q
+// receives, from every Fourier-side slab r, the block of its n3/P planes
+// (fwd: Ub[q][r] = U[r][q]; back: U[r][q] = Ub[q][r]; blocks of nvec 3 nblk).
+cudaError_t slab_exchange(bnf_solver* s, double2* U, double2* Ub, int nvec, int fwd, cudaStream_t st) {
+    const int P = s->nsl;
+    const size_t nloc = (size_t)(s->n / P), blk = (size_t)nvec * 3 * (nloc / P), part = (size_t)nvec * 3 * nloc;
+    for (int q = 0; q < P; ++q)
+        for (int r = 0; r < P; ++r) {
+            double2* u = U + r * part + q * blk;
+            double2* b = Ub + q * part + r * blk;
+            cudaError_t e = cudaMemcpyAsync(fwd ? b : u, fwd ? u : b, blk * sizeof(double2), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return e;
+        }
+    return cudaSuccess;
+}
+
+const char* plane_name(const OpArgs& a, bool cg) {
+    if (a.plane_w) return a.plane_w == 2 ? (cg ? "plane_ws_cg" : "plane_ws") : (cg ? "plane_w_cg" : "plane_w");
+    if (a.plane_l2) return cg ? "plane_l2_cg" : "plane_l2";
+    return cg ? "plane_cg" : "plane";
 }
 
 // out = op(y) for nvec vectors (device pointers, 2n each)
 int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     TRY(ensure_work(s, nvec));
     double2* U = s->U.as<double2>();
+    if (s->nsl > 1) {   // virtual slabs: z pass per j-slab, exchange, plane per z-slab, exchange, adjoint z pass
+        const int P = s->nsl;
+        const size_t nloc = (size_t)(s->n / P), part = (size_t)nvec * 3 * nloc;
+        double2* Ub = s->Ub.as<double2>();
+        for (int r = 0; r < P; ++r)
+            RUN("zfwd2", launch_zfwd2(slab_args(s, r), y + r * 2 * nloc, U + r * part, nvec, op, nullptr, nullptr, nullptr,
+                                      s->st));
+        RUN("slab_a2a", slab_exchange(s, U, Ub, nvec, 1, s->st));
+        for (int q = 0; q < P; ++q)
+            RUN(plane_name(s->args, false), launch_plane(slab_args(s, q), Ub + q * part, 3 * nvec, nullptr, s->st));
+        RUN("slab_a2a", slab_exchange(s, U, Ub, nvec, 0, s->st));
+        for (int r = 0; r < P; ++r)
+            RUN("zadj2", launch_zadj2(slab_args(s, r), U + r * part, out + r * 2 * nloc, nvec, op, nullptr, s->st));
+        s->matvecs += nvec;
+        return BNF_OK;
+    }
     if (s->use_z2) RUN("zfwd2", launch_zfwd2(s->args, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
-        RUN(s->args.plane_w ? (s->args.plane_w == 2 ? "plane_ws" : "plane_w") : s->args.plane_l2 ? "plane_l2" : "plane",
-            launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+        RUN(plane_name(s->args, false), launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
     } else {
         RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
@@ -461,6 +523,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
     // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2,
     // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles)
     const int nvar = plane_w_supported(s->args) ? 5 : 3;
+    const int v0 = s->nsl > 1 ? 2 : 0;   // slab mode: plane passes through L2 only (slab-aware)
     float best[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
@@ -470,7 +533,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
         s->args.plane_l2 = variant == 2 ? 1 : 0;
         s->args.plane_w = variant >= 3 ? variant - 2 : 0;
     };
-    for (int variant = 0; variant < nvar; ++variant) {
+    for (int variant = v0; variant < nvar; ++variant) {
         set(variant);
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
         CK(cudaEventRecord(e0, s->st));
@@ -479,8 +542,8 @@ int autotune_plane(bnf_solver* s, int nvec) {
         CK(cudaEventSynchronize(e1));
         CK(cudaEventElapsedTime(&best[variant], e0, e1));
     }
-    int pick = 0;
-    for (int variant = 1; variant < nvar; ++variant)
+    int pick = v0;
+    for (int variant = v0 + 1; variant < nvar; ++variant)
         if (best[variant] < best[pick]) pick = variant;
     set(pick);
     s->matvecs = mv0;
@@ -563,6 +626,23 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
         if (e != cudaSuccess) return e;   \
         ++k;                              \
     } while (0)
+    if (s->nsl > 1) {   // virtual slabs: per-slab passes, device-copy all-to-alls
+        const int NS = s->nsl;
+        const size_t nloc = (size_t)(s->n / NS), part = (size_t)nvec * 3 * nloc;
+        double2* Ub = s->Ub.as<double2>();
+        for (int r = 0; r < NS; ++r)
+            BNF_K(launch_zfwd2(slab_args(s, r), R + r * 2 * nloc, U + r * part, nvec, 1, P + r * 2 * nloc,
+                               X + r * 2 * nloc, &cg, st));
+        BNF_K(slab_exchange(s, U, Ub, nvec, 1, st));
+        for (int q = 0; q < NS; ++q) BNF_K(launch_plane(slab_args(s, q), Ub + q * part, 3 * nvec, &cg, st));
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        BNF_K(slab_exchange(s, U, Ub, nvec, 0, st));
+        for (int r = 0; r < NS; ++r)
+            BNF_K(launch_zadj2(slab_args(s, r), U + r * part, R + r * 2 * nloc, nvec, 1, &cg, st));
+        BNF_K(launch_cg_finish(cg, 1, nvec, st));
+        *nk = k;
+        return cudaSuccess;
+    }
     if (s->use_z2) BNF_K(launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, st));
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
@@ -684,12 +764,15 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
         cg.iter = nullptr;
         for (; it < s->o.max_inner; ++it) {
             // eager: one timed launch per pass (profiling, bnf_kernel_times)
+            if (s->nsl > 1) {
+                int nk = 0;
+                RUN("cg_iter_slabs", cg_iter_kernels(s, cg, R, P, U, X, nvec, s->st, &nk));
+                s->prof.launches += nk - 1;
+            } else {
             if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
-                RUN(s->args.plane_w ? (s->args.plane_w == 2 ? "plane_ws_cg" : "plane_w_cg")
-                                    : s->args.plane_l2 ? "plane_l2_cg" : "plane_cg",
-                    launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+                RUN(plane_name(s->args, true), launch_plane(s->args, U, 3 * nvec, &cg, s->st));
                 RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
@@ -700,6 +783,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
             else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
             RUN("cg_beta", launch_cg_finish(cg, 1, nvec, s->st));
+            }
             s->matvecs += nvec;
             CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
             CK(cudaStreamSynchronize(s->st));
@@ -723,10 +807,10 @@ int apply_Ar_inv(bnf_solver* s, const double2* X, double2* Y, int nvec) {
     const long long N = 2 * s->n;
     CK(s->cgc.ensure((size_t)N * nvec * sizeof(double2)));
     double2* C = s->cgc.as<double2>();
-    RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->n, nvec, 1, s->st));
+    RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->n, nvec, 1, s->st, s->n / s->nsl));
     if (s->fused_ok) TRY(cg_solve_fused(s, C, Y, nvec, nullptr));
     else TRY(cg_solve(s, C, Y, nvec, nullptr));
-    RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->n, nvec, 1, s->st));
+    RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->n, nvec, 1, s->st, s->n / s->nsl));
     return BNF_OK;
 }
 
@@ -859,7 +943,7 @@ int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
         }
         p.gamma = i0 + (long long)n1 * (j0 + (long long)n2 * k0);
     }
-    RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st));
+    RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st, 0, s->L.n[1] / s->nsl, s->n));
     s->kappa_set = true;
     s->kver++;
     return BNF_OK;
@@ -1001,6 +1085,7 @@ void bnf_opts_default(bnf_opts* o) {
     o->reorth_once_ok = 1;
     o->res_tol = 5e-9;
     o->max_polish = 3;
+    o->slabs = 1;
 }
 
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
@@ -1093,6 +1178,14 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     p.gamma = -1;
     p.taup = 1e-6;
     s->args.inv_n = 1.0 / (double)n;
+    s->args.j0 = 0;           // whole grid: one slab
+    s->args.n2loc = n2;
+    s->args.n3loc = n3;
+    s->args.slab = 0;
+    s->args.nslab = 1;
+    s->args.nloc = n;
+    s->args.vsf = 2 * n;
+    s->args.nblk = n;
     s->args.fast = (std::getenv("BNF_NO_FAST") == nullptr) ? 1 : 0;
     // tile widths: keep each kernel's shared memory <= ~100 KB
     const int budget = 100 * 1024;
@@ -1131,6 +1224,18 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
+    // virtual slabs (SURVEY §8(e) / DESIGN §8): the slab-decomposed operator with the
+    // all-to-alls as device copies; needs the fast z passes and an L2 plane middle
+    s->nsl = std::max(1, o.slabs);
+    if (s->nsl > 1) {
+        const int P = s->nsl;
+        if (n2 % P != 0 || n3 % P != 0 || !s->use_z2 || !s->plane_ok || !plane_w_supported(s->args) ||
+            std::getenv("BNF_NO_PLANE") != nullptr || (std::getenv("BNF_PLANE") && !std::getenv("BNF_PLANE_L2"))) {
+            set_error("opts.slabs > 1 needs n2 and n3 divisible by slabs, a square xy plane of 64, 128 or 256 and the "
+                      "fused z passes / L2 plane pass");
+            return BNF_EINVAL;
+        }
+    }
     s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
@@ -1216,6 +1321,21 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
             lastk = k;
         }
         idx[t] = (unsigned char)lastk;
+    }
+    if (s->nsl > 1) {   // slab-major [slab][l][cl][b][a] (real-space z-slabs of n3 / P planes)
+        const int P = s->nsl;
+        const long long plane = (long long)s->L.n[0] * s->L.n[1], n = s->n, nloc = n / P, n3l = s->L.n[2] / P;
+        std::vector<double> h2(n3);
+        std::vector<unsigned char> i2(small ? n3 : 0);
+        for (int q = 0; q < P; ++q)
+            for (int l = 0; l < 3; ++l)
+                for (long long cl = 0; cl < n3l; ++cl) {
+                    const long long src = l * n + (q * n3l + cl) * plane, dst = (long long)q * 3 * nloc + l * nloc + cl * plane;
+                    std::memcpy(h2.data() + dst, h.data() + src, plane * sizeof(double));
+                    if (small) std::memcpy(i2.data() + dst, idx.data() + src, plane);
+                }
+        h.swap(h2);
+        if (small) idx.swap(i2);
     }
     CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), n3 * sizeof(double), cudaMemcpyHostToDevice, s->st));
     s->args.eps_idx = nullptr;
@@ -1338,7 +1458,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     CK(s->small.ensure((size_t)(64 + 8 * std::max<long long>((long long)(maxsteps + 1) * b, want)) * sizeof(double2)));
     double2* V = s->V.as<double2>();
     // start block: seeded counter-based normals, Gamma mode masked (R6)
-    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st));
+    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st, s->n / s->nsl));
     if (s->o.warm && s->prev_want > 0) {
         // Warm start (DESIGN R17): start block = fixed pseudo-random combinations of
         // the previous solve's Ritz vectors (neighbouring k on the path) plus 1e-3 of
@@ -1354,8 +1474,8 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
             x = cd(((double)(h >> 11) / 9007199254740992.0) - 0.5, 0.0);
         }
         TRY(gemm_nn_host(s, s->Yv.as<double2>(), pw, Wm, b, V, 1.0, 1e-3));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st, s->n / s->nsl));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st, s->n / s->nsl));
     }
     bool ok = true;
     std::vector<cd> R0;
@@ -1420,7 +1540,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         TRY(chol_qr2(s, W, b, Rn, ok));
         if (!ok) {  // invariant subspace / breakdown: continue with a fresh random block
             RUN("fill_random", launch_fill_random(W, N, b, s->o.seed + 7919ull * (step + 1), 0,
-                                                  s->sigma.as<double>(), s->n, s->st));
+                                                  s->sigma.as<double>(), s->n, s->st, s->n / s->nsl));
             for (int pass = 0; pass < 2; ++pass) {
                 TRY(gram_host(s, V, p, W, b, H));
                 TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
@@ -1603,6 +1723,10 @@ int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
         CK(cudaMemcpyAsync(out, s->Yv.p, (size_t)N * nev * sizeof(double2), dir, s->st));
         CK(cudaStreamSynchronize(s->st));
         return BNF_OK;
+    }
+    if (s->nsl > 1) {
+        set_error("BNF_VEC_E is not available with opts.slabs > 1 (fetch BNF_VEC_Y, slab layout)");
+        return BNF_EINVAL;
     }
     // e = B^{-1} Q_r Sigma_r y / sqrt(lambda), Bloch phase of eq. (T) included
     const long long n = s->n;

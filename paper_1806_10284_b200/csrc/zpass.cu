@@ -58,6 +58,18 @@ __device__ __forceinline__ double2 cadd3(double2 a, double2 b, double2 c) {
     return make_double2(a.x + b.x + c.x, a.y + b.y + c.y);
 }
 
+// Real-space side of the z passes in slab-major order [q][vec][l][cl][jl][i]
+// (c = q n3loc + cl; q = the z-slab the rows are sent to; blocks
+// of nblk = n1 n2loc n3loc elements); with one slab this is the plain
+// [vec][l][c][j][i].  Offset of row c of
+// component l of vector vec, relative to the column (jl, i) offset.
+template <int SL>
+__device__ __forceinline__ size_t u_row(const OpArgs& a, int nvec, int vec, int l, int c, size_t kstride) {
+    if constexpr (SL == 0) return ((size_t)vec * 3 + l) * a.nloc + kstride * (size_t)c;
+    const int q = c / a.n3loc, cl = c - q * a.n3loc;
+    return (((size_t)q * nvec + vec) * 3 + l) * a.nblk + kstride * (size_t)cl;
+}
+
 template <int N1, int N2, int W>
 struct ZCfg {
     static constexpr int N = N1 * N2;
@@ -77,7 +89,7 @@ struct ColS {   // per-column constants shared through smem
 // CTAs per SM overlap one tile's loads with the other's FP64 work.  The
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
-template <int N1, int N2, int W, int MODE>
+template <int N1, int N2, int W, int MODE, int SL = 0>
 __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
@@ -86,15 +98,16 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     extern __shared__ double2 sm[];   // [NA][TE]: y1 y2 (+1) | r1 r2 p1 p2; Ct = [0..3)
     __shared__ ColS cs[W];
     const ModeP& p = a.mp;
-    const long long n = p.n;
+    const long long n = a.nloc;                         // per-component stride on this slab
     const int n1 = p.n1;
-    const size_t kstride = (size_t)n1 * p.n2;
+    const size_t kstride = (size_t)n1 * a.n2loc;       // local k stride (j-slab)
+    const long long kglob = (long long)n1 * p.n2;      // global k stride (mode index)
     const int tid = threadIdx.x;
-    const int i0 = blockIdx.x * W, j = blockIdx.y, vec = blockIdx.z;
-    const size_t col0 = (size_t)i0 + (size_t)n1 * j;
+    const int i0 = blockIdx.x * W, j = blockIdx.y + a.j0, vec = blockIdx.z;
+    const size_t col0 = (size_t)i0 + (size_t)n1 * blockIdx.y;
     {
-        const double2* y1 = Y + (size_t)vec * 2 * n + col0;
-        const double2* p1 = MODE ? Pcg + (size_t)vec * 2 * n + col0 : nullptr;
+        const double2* y1 = Y + (size_t)vec * a.vsf + col0;
+        const double2* p1 = MODE ? Pcg + (size_t)vec * a.vsf + col0 : nullptr;
 #pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
             const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
     // x is streamed straight from HBM (not staged), one element ahead
-    double2* xcol = MODE ? Xcg + (size_t)vec * 2 * n + gcol : nullptr;
+    double2* xcol = MODE ? Xcg + (size_t)vec * a.vsf + gcol : nullptr;
     double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0);
     if (MODE == 1 && tid < TE) {
         xn1 = xcol[kstride * (tid / W)];
@@ -143,13 +156,13 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
             xg[n] = make_double2(fma(alpha_prev, q2.x, x2.x), fma(alpha_prev, q2.y, x2.y));
             u1 = make_double2(fma(beta, q1.x, u1.x), fma(beta, q1.y, u1.y));   // p <- r + beta p
             u2 = make_double2(fma(beta, q2.x, u2.x), fma(beta, q2.y, u2.y));
-            double2* pg = Pcg + (size_t)vec * 2 * n + gcol + kstride * k;
+            double2* pg = Pcg + (size_t)vec * a.vsf + gcol + kstride * k;
             pg[0] = u1;
             pg[n] = u2;
         }
         const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
         Coef o;
-        const long long idx = c.cm.idx0 + (long long)kstride * k;
+        const long long idx = c.cm.idx0 + kglob * k;
         modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
         const double2 U1 = cscale(u1, o.f1), U2 = cscale(u2, o.f2);
         sm[e] = modes::comb(o, 0, U1, U2);           // component tiles alias the consumed inputs
@@ -170,18 +183,19 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
         const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
         const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
         const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
-        double2* out = U + (size_t)vec * 3 * n + (size_t)l * n + gcol;
+        double2* out = U + gcol;
         fast::twiddle_stage2<N1, N2>(v, wt, wu, wk);
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) out[kstride * (t + N2 * u + N1 * k2)] = v[u * N2 + k2];
+            for (int k2 = 0; k2 < N2; ++k2)
+                out[u_row<SL>(a, gridDim.z, vec, l, t + N2 * u + N1 * k2, kstride)] = v[u * N2 + k2];
     }
 }
 
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
-template <int N1, int N2, int W, int MODE>
+template <int N1, int N2, int W, int MODE, int SL = 0>
 __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
@@ -190,20 +204,22 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     __shared__ ColS cs[W];
     __shared__ double2 red[32];
     const ModeP& p = a.mp;
-    const long long n = p.n;
+    const long long n = a.nloc;
     const int n1 = p.n1;
-    const size_t kstride = (size_t)n1 * p.n2;
+    const size_t kstride = (size_t)n1 * a.n2loc;
+    const long long kglob = (long long)n1 * p.n2;
     const int tid = threadIdx.x;
-    const int i0 = blockIdx.x * W, j = blockIdx.y, vec = blockIdx.z;
-    const size_t col0 = (size_t)i0 + (size_t)n1 * j;
+    const int i0 = blockIdx.x * W, j = blockIdx.y + a.j0, vec = blockIdx.z;
+    const size_t col0 = (size_t)i0 + (size_t)n1 * blockIdx.y;
     {
-        const double2* u0 = U + (size_t)vec * 3 * n + col0;
+        const double2* u0 = U + col0;
 #pragma unroll 2
         for (int q = tid; q < TE; q += NT) {
-            const size_t g = (size_t)(q % W) + kstride * (size_t)(q / W);
-            cp_async16(sm + q, u0 + g);
-            cp_async16(sm + TE + q, u0 + n + g);
-            cp_async16(sm + 2 * TE + q, u0 + 2 * n + g);
+            const int c = q / W;
+            const size_t g = (size_t)(q % W);
+            cp_async16(sm + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 0, c, kstride));
+            cp_async16(sm + TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 1, c, kstride));
+            cp_async16(sm + 2 * TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 2, c, kstride));
         }
         cp_async_commit();
     }
@@ -218,7 +234,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     const int w = tid % W;
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
-    double2* o1 = OUT + (size_t)vec * 2 * n + gcol;
+    double2* o1 = OUT + (size_t)vec * a.vsf + gcol;
     double2 rn1 = make_double2(0, 0), rn2 = make_double2(0, 0);
     if (MODE == 1 && tid < TE) {   // first residual element, in flight during the FFT phase
         rn1 = o1[kstride * (tid / W)];
@@ -250,7 +266,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
         const int k = e / W;
         const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
         Coef o;
-        const long long idx = c.cm.idx0 + (long long)kstride * k;
+        const long long idx = c.cm.idx0 + kglob * k;
         modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
         const double2 w0 = sm[e], w1 = sm[TE + e], w2 = sm[2 * TE + e];
         double2 z1 = cadd3(cjm(o.num1[0], w0), cjm(o.num1[1], w1), cjm(o.num1[2], w2));
@@ -275,9 +291,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     }
     if (MODE == 1) {
         // per-CTA partial of (r, r); beta is formed by k_cg_finish after this pass
+        // partials of every slab of a vector are contiguous: [vec][slab][block]
         const int nb = gridDim.x * gridDim.y;
-        cg_block_partial(rr, cg.part_z + (size_t)vec * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x, red);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb;
+        cg_block_partial(rr, cg.part_z + ((size_t)vec * a.nslab + a.slab) * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x,
+                         red);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb * a.nslab;
     }
 }
 
@@ -323,19 +341,17 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_fwd(mode);
-    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
-    if (mode) {
-        auto kern = k_zfwd2<N1, N2, W, 1>;
+    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
+    auto go = [&](auto kern, int opv, double2* Pp, double2* Xp, CGFuse cgv) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<g, L::C::NT, smem, st>>>(Y, U, a, 1, P, X, *cg);
-    } else {
-        auto kern = k_zfwd2<N1, N2, W, 0>;
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        kern<<<g, L::C::NT, smem, st>>>(Y, U, a, op, nullptr, nullptr, CGFuse{});
-    }
-    return cudaGetLastError();
+        kern<<<g, L::C::NT, smem, st>>>(Y, U, a, opv, Pp, Xp, cgv);
+        return cudaGetLastError();
+    };
+    const bool sl = a.nslab > 1;
+    if (mode) return sl ? go(k_zfwd2<N1, N2, W, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0>, 1, P, X, *cg);
+    return sl ? go(k_zfwd2<N1, N2, W, 0, 1>, op, nullptr, nullptr, CGFuse{})
+              : go(k_zfwd2<N1, N2, W, 0, 0>, op, nullptr, nullptr, CGFuse{});
 }
 
 template <int N1, int N2, int W>
@@ -344,19 +360,16 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
     const size_t smem = L::smem_adj(mode);
-    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.mp.n2, (unsigned)nvec);
-    if (mode) {
-        auto kern = k_zadj2<N1, N2, W, 1>;
+    const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
+    auto go = [&](auto kern, int opv, CGFuse cgv) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, 1, *cg);
-    } else {
-        auto kern = k_zadj2<N1, N2, W, 0>;
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, op, CGFuse{});
-    }
-    return cudaGetLastError();
+        kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, opv, cgv);
+        return cudaGetLastError();
+    };
+    const bool sl = a.nslab > 1;
+    if (mode) return sl ? go(k_zadj2<N1, N2, W, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0>, 1, *cg);
+    return sl ? go(k_zadj2<N1, N2, W, 0, 1>, op, CGFuse{}) : go(k_zadj2<N1, N2, W, 0, 0>, op, CGFuse{});
 }
 
 // n3 -> (N1, N2, W)

@@ -10,9 +10,6 @@
 
 using namespace bnf::fast;
 
-__device__ __forceinline__ double2 shfl_xor2(double2 v, int d) {
-    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, d), __shfl_xor_sync(0xffffffffu, v.y, d));
-}
 
 // N2 x N2 transposes (one per u) across the N2 consecutive lanes of a sequence:
 // element (lane t, slot u*N2 + s) -> (lane s, slot u*N2 + t)

@@ -553,3 +553,74 @@ def test_cg_solve_converges_to_tolerance(bnf):
     x = xd.cpu().numpy()[0]
     r = np.linalg.norm(c[0] - op.M(x)) / np.linalg.norm(c[0])
     assert 0 < it < 2000 and r <= 2e-13, (it, r)
+
+
+# ------------------------------------------------ slab decomposition (SURVEY §8(e))
+def _to_slab(y, n, P):
+    """[b][half][k][j][i] -> the slab layout [b][slab][half][k][jl][i] (bnf_opts.slabs)."""
+    n1, n2, n3 = n
+    b = y.shape[0]
+    return np.ascontiguousarray(y.reshape(b, 2, n3, P, n2 // P, n1).transpose(0, 3, 1, 2, 4, 5)).reshape(b, -1)
+
+
+def _from_slab(y, n, P):
+    n1, n2, n3 = n
+    b = y.shape[0]
+    return np.ascontiguousarray(y.reshape(b, P, 2, n3, n2 // P, n1).transpose(0, 2, 3, 1, 4, 5)).reshape(b, -1)
+
+
+@pytest.mark.parametrize("idx,n,P,middle", [(2, (64, 64, 64), 2, "l2"), (2, (64, 64, 64), 4, "warp_smem"),
+                                            (4, (128, 128, 128), 2, "warp_shfl"), (5, None, 2, "l2"),
+                                            (5, None, 4, "warp_smem")])
+def test_virtual_slabs_operator_equals_whole_grid(bnf, monkeypatch, idx, n, P, middle):
+    """The slab-decomposed operator (Fourier side split over j, real side over
+    z-planes, the all-to-all as device copies; bnf_opts.slabs = P) equals the
+    whole-grid operator to 1e-13 (same FFT arithmetic, different data layout)
+    for A_r and M, b = 2, and the oracle's operator to OP_TOL."""
+    cfg, n, kap = _cfg_case(idx, n, 3 if idx != 5 else 0)
+    L, O, eps, S1 = _forced_solver(bnf, monkeypatch, MIDDLES[middle], cfg, n)
+    _, _, _, SP = _forced_solver(bnf, monkeypatch, MIDDLES[middle], cfg, n, slabs=P)
+    y = vectors.complex_normal((2, 2 * O.nn), seed=31)
+    op = fftop.NFSEPOperator(O, kap, eps)
+    sel = np.random.default_rng(1).choice(2 * O.nn, 4096, replace=False)
+    for code, name in ((bnf.OP_AR, "Ar"), (bnf.OP_M, "M")):
+        whole = _apply_gpu(S1, kap, y, code)
+        slab = _from_slab(_apply_gpu(SP, kap, _to_slab(y, n, P), code), n, P)
+        assert np.abs(slab - whole).max() <= 1e-13 * np.abs(whole).max(), (name, P)
+        want = op.apply(y[0], name)
+        assert np.abs(slab[0][sel] - want[sel]).max() <= OP_TOL * np.abs(want).max()
+    S1.close()
+    SP.close()
+
+
+def test_virtual_slabs_eigenvalues(bnf):
+    """A full solve on P = 2 virtual slabs (CG-fused passes per slab, partial sums
+    of both slabs in the CG scalars, Lanczos on slab-layout vectors) returns the
+    whole-grid eigenvalues to 1e-10 (config 2 lattice and eps at 64^3, k 9 golden)."""
+    g = _golden(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"), "full_c2_k9_oracle.json")
+    cfg = configs.config(2)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape, slabs=2)
+    lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
+    assert st["converged"] == 1
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+    Y = np.zeros((len(lam), 2 * O.nn), dtype=np.complex128)
+    S.eigvecs(bnf.VEC_Y, Y)
+    op = fftop.NFSEPOperator(O, tuple(g["kappa"]), eps)
+    Yw = _from_slab(Y, tuple(g["n"]), 2)
+    for i in range(3):
+        r = np.linalg.norm(op.Ar(Yw[i]) - lam[i] * Yw[i]) / np.linalg.norm(Yw[i])
+        assert r <= 1e-8
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_virtual_slabs_config5_golden(bnf, golden_dir, P):
+    """Config 5 (FCC diamond 256^3, one k) on P virtual slabs: eigenvalues equal
+    the oracle golden (tests/golden/full_c5_k0_oracle.json) to 1e-10."""
+    path = os.path.join(golden_dir, "full_c5_k0_oracle.json")
+    if not os.path.exists(path):
+        pytest.skip("config-5 oracle golden not generated")
+    g = _golden(golden_dir, "full_c5_k0_oracle.json")
+    cfg = configs.config(5)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape, slabs=P)
+    lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
