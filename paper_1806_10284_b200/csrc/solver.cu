@@ -1186,6 +1186,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.nloc = n;
     s->args.vsf = 2 * n;
     s->args.nblk = n;
+    s->args.zcfg = std::getenv("BNF_ZCFG") ? std::atoi(std::getenv("BNF_ZCFG")) : 0;
     s->args.fast = (std::getenv("BNF_NO_FAST") == nullptr) ? 1 : 0;
     // tile widths: keep each kernel's shared memory <= ~100 KB
     const int budget = 100 * 1024;

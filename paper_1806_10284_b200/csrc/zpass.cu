@@ -71,6 +71,11 @@ __device__ __forceinline__ size_t u_row(const OpArgs& a, int nvec, int vec, int 
 }
 
 template <int N1, int N2, int W>
+struct ZCfg;
+// resident CTAs per SM the z passes are compiled for (register budget)
+constexpr int z_minb(int nt) { return nt > 256 ? 2 : (nt <= 96 ? 5 : BNF_Z_MINB); }
+
+template <int N1, int N2, int W>
 struct ZCfg {
     static constexpr int N = N1 * N2;
     static constexpr int NT = 3 * W * N2;
@@ -89,8 +94,8 @@ struct ColS {   // per-column constants shared through smem
 // CTAs per SM overlap one tile's loads with the other's FP64 work.  The
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
-template <int N1, int N2, int W, int MODE, int SL = 0>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
+template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::NT))
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
@@ -116,6 +121,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
             if (MODE == 1) {
                 cp_async16(sm + 2 * TE + q, p1 + g);
                 cp_async16(sm + 3 * TE + q, p1 + n + g);
+                if (RST) {   // x staged too: every input of the tile in flight at once
+                    const double2* x1 = Xcg + (size_t)vec * a.vsf + col0;
+                    cp_async16(sm + 4 * TE + q, x1 + g);
+                    cp_async16(sm + 5 * TE + q, x1 + n + g);
+                }
             }
         }
         cp_async_commit();
@@ -135,7 +145,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     // x is streamed straight from HBM (not staged), one element ahead
     double2* xcol = MODE ? Xcg + (size_t)vec * a.vsf + gcol : nullptr;
     double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0);
-    if (MODE == 1 && tid < TE) {
+    if (MODE == 1 && !RST && tid < TE) {
         xn1 = xcol[kstride * (tid / W)];
         xn2 = xcol[n + kstride * (tid / W)];
     }
@@ -146,8 +156,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
         double2 u1 = sm[e], u2 = sm[TE + e];
         if (MODE == 1) {
             const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
-            const double2 x1 = xn1, x2 = xn2;
-            if (e + NT < TE) {
+            const double2 x1 = RST ? sm[4 * TE + e] : xn1, x2 = RST ? sm[5 * TE + e] : xn2;
+            if (!RST && e + NT < TE) {
                 xn1 = xcol[kstride * ((e + NT) / W)];
                 xn2 = xcol[n + kstride * ((e + NT) / W)];
             }
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
         for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
         __syncthreads();
         fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
-        const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+        const unsigned long long nn = (unsigned long long)p.n, N3 = c.base3;   // e^{2 pi i P / n}: global n
         const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
         const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
         const double2 wk = tw_at(a.tw, ((unsigned long long)N1 * N3) % nn);
@@ -195,8 +205,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
 
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
-template <int N1, int N2, int W, int MODE, int SL = 0>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256 ? 2 : BNF_Z_MINB)
+template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::NT))
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
@@ -220,6 +230,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
             cp_async16(sm + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 0, c, kstride));
             cp_async16(sm + TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 1, c, kstride));
             cp_async16(sm + 2 * TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 2, c, kstride));
+            if (MODE == 1 && RST) {   // residual tile staged with U: every load of the tile in flight at once
+                const double2* r0 = OUT + (size_t)vec * a.vsf + col0 + g + kstride * (size_t)c;
+                cp_async16(sm + 3 * TE + q, r0);
+                cp_async16(sm + 4 * TE + q, r0 + n);
+            }
         }
         cp_async_commit();
     }
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     const size_t gcol = col0 + w;
     double2* o1 = OUT + (size_t)vec * a.vsf + gcol;
     double2 rn1 = make_double2(0, 0), rn2 = make_double2(0, 0);
-    if (MODE == 1 && tid < TE) {   // first residual element, in flight during the FFT phase
+    if (MODE == 1 && !RST && tid < TE) {   // first residual element, in flight during the FFT phase
         rn1 = o1[kstride * (tid / W)];
         rn2 = o1[n + kstride * (tid / W)];
     }
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
     {
         const int l = tid / (W * N2), t = (tid / W) % N2;
         double2* ct = sm + (size_t)l * TE;
-        const unsigned long long nn = (unsigned long long)n, N3 = c.base3;
+        const unsigned long long nn = (unsigned long long)p.n, N3 = c.base3;   // e^{2 pi i P / n}: global n
         const double2 wt = conj2(tw_at(a.tw, ((unsigned long long)t * N3) % nn));
         const double2 wu = conj2(tw_at(a.tw, ((unsigned long long)N2 * N3) % nn));
         double2 v[N1];
@@ -274,8 +289,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, ZCfg<N1, N2, W>::NT > 256
         z1 = cscale(z1, o.f1);
         z2 = cscale(z2, o.f2);
         if (MODE == 1) {
-            double2 r1 = rn1, r2 = rn2;
-            if (e + NT < TE) {
+            double2 r1 = RST ? sm[3 * TE + e] : rn1, r2 = RST ? sm[4 * TE + e] : rn2;
+            if (!RST && e + NT < TE) {
                 rn1 = o1[kstride * ((e + NT) / W)];
                 rn2 = o1[n + kstride * ((e + NT) / W)];
             }
@@ -317,8 +332,8 @@ __global__ void k_cg_xfinal(double2* __restrict__ X, const double2* __restrict__
 template <int N1, int N2, int W>
 struct ZLaunch {
     using C = ZCfg<N1, N2, W>;
-    static size_t smem_fwd(int mode) { return (size_t)(mode ? 4 : 3) * C::TE * sizeof(double2); }
-    static size_t smem_adj(int) { return (size_t)3 * C::TE * sizeof(double2); }
+    static size_t smem_fwd(int mode, int rst) { return (size_t)(mode ? (rst ? 6 : 4) : 3) * C::TE * sizeof(double2); }
+    static size_t smem_adj(int mode, int rst) { return (size_t)(mode && rst ? 5 : 3) * C::TE * sizeof(double2); }
 };
 
 }  // namespace
@@ -340,7 +355,8 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
                            const CGFuse* cg, cudaStream_t st) {
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
-    const size_t smem = L::smem_fwd(mode);
+    const int rst = (a.zcfg & 1) && mode;
+    const size_t smem = L::smem_fwd(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, double2* Pp, double2* Xp, CGFuse cgv) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -349,6 +365,7 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if (mode && rst) return sl ? go(k_zfwd2<N1, N2, W, 1, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0, 1>, 1, P, X, *cg);
     if (mode) return sl ? go(k_zfwd2<N1, N2, W, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0>, 1, P, X, *cg);
     return sl ? go(k_zfwd2<N1, N2, W, 0, 1>, op, nullptr, nullptr, CGFuse{})
               : go(k_zfwd2<N1, N2, W, 0, 0>, op, nullptr, nullptr, CGFuse{});
@@ -359,7 +376,8 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
                            cudaStream_t st) {
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
-    const size_t smem = L::smem_adj(mode);
+    const int rst = (a.zcfg & 1) && mode;
+    const size_t smem = L::smem_adj(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, CGFuse cgv) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -368,15 +386,24 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if (mode && rst) return sl ? go(k_zadj2<N1, N2, W, 1, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0, 1>, 1, *cg);
     if (mode) return sl ? go(k_zadj2<N1, N2, W, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0>, 1, *cg);
     return sl ? go(k_zadj2<N1, N2, W, 0, 1>, op, CGFuse{}) : go(k_zadj2<N1, N2, W, 0, 0>, op, CGFuse{});
 }
 
 // n3 -> (N1, N2, W)
 #define BNF_Z2_PLANS(X) X(64, 8, 8, 16) X(96, 24, 4, 8) X(128, 16, 8, 8) X(192, 24, 8, 4) X(256, 16, 16, 4)
+// narrower tiles (zcfg bit 1): more resident CTAs per SM
+#define BNF_Z2_HALF(X) X(64, 8, 8, 8) X(128, 16, 8, 4) X(256, 16, 16, 2)
 
 cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, double2* P, double2* X,
                          const CGFuse* cg, cudaStream_t st) {
+    if (a.zcfg & 2) switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: if (a.mp.n1 % WW == 0) return zfwd2_t<A, B, WW>(a, Y, U, nvec, op, P, X, cg, st); break;
+        BNF_Z2_HALF(BNF_CASE)
+#undef BNF_CASE
+        default: break;
+    }
     switch (a.mp.n3) {
 #define BNF_CASE(NN, A, B, WW) case NN: return zfwd2_t<A, B, WW>(a, Y, U, nvec, op, P, X, cg, st);
         BNF_Z2_PLANS(BNF_CASE)
@@ -387,6 +414,12 @@ cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec
 
 cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,
                          cudaStream_t st) {
+    if (a.zcfg & 2) switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: if (a.mp.n1 % WW == 0) return zadj2_t<A, B, WW>(a, U, OUT, nvec, op, cg, st); break;
+        BNF_Z2_HALF(BNF_CASE)
+#undef BNF_CASE
+        default: break;
+    }
     switch (a.mp.n3) {
 #define BNF_CASE(NN, A, B, WW) case NN: return zadj2_t<A, B, WW>(a, U, OUT, nvec, op, cg, st);
         BNF_Z2_PLANS(BNF_CASE)
