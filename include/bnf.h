@@ -53,7 +53,7 @@ extern "C" {
 #define BNF_EGEOM 2     /* P:L143 admissibility violated after canonicalisation, or degenerate snapped cell */
 #define BNF_ENOMEM 3    /* device or host allocation failed */
 #define BNF_ECUDA 4     /* CUDA runtime error (no device, launch failure, ...) */
-#define BNF_ENCCL 5     /* reserved: distributed (slab) mode */
+#define BNF_ENCCL 5     /* NCCL failure or libnccl.so.2 not loadable (distributed slab mode) */
 #define BNF_ENOCONV 6   /* eigensolver did not reach tolerance; partial results + residuals in stats */
 #define BNF_ESTATE 7    /* call order violated (e.g. solve before bnf_set_epsilon) */
 
@@ -179,6 +179,26 @@ typedef struct {
    factor > 31 or exceeds 1024. */
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out);
 void bnf_solver_destroy(bnf_solver* s);
+
+/* Distributed slab mode (one k-point on several GPUs,
+   one process per GPU; §5.3 Algorithms 1-2 with the 3D transforms
+   split).  nranks processes each own one slab: the Fourier side of every
+   vector is split over j (rank r holds j in [r n2/P, (r+1) n2/P), all i, k:
+   local vectors of 2n/P complex laid out [half][k][jl][i]), the real-space
+   work over z-planes (rank r holds n3/P planes).  Per operator application
+   two all-to-alls (NCCL send/recv groups, 3 nvec n/P^2 complex per rank pair)
+   move the real-space blocks; the CG partial sums are all-gathered and the
+   Lanczos Gram products all-reduced, so every rank holds the same small
+   matrices and returns the same eigenvalues.  Needs n2, n3 divisible by
+   nranks and the fast square-plane path (as opts.slabs).  `id` is the NCCL
+   unique id of the group (bnf_nccl_unique_id on one rank, broadcast by the
+   caller); opts.device is this rank's GPU.  bnf_set_epsilon takes the full
+   3n field (each rank keeps its slab); bnf_apply_Ar / BNF_VEC_Y use local
+   vectors; BNF_VEC_E is refused.  Every rank must make the same calls in the
+   same order (collectives).  BNF_ENCCL on an NCCL error. */
+int bnf_nccl_unique_id(unsigned char id[128]);
+int bnf_solver_create_dist(const bnf_lattice* lat, const bnf_opts* opts, int nranks, int rank, const unsigned char id[128],
+                           bnf_solver** out);
 
 /* Permittivity B: eps[3n] = [vec B1; vec B2; vec B3], real-space
    layout, every value > 0 (BNF_EINVAL otherwise).  mem = BNF_MEM_HOST or

@@ -69,6 +69,8 @@ _sigs = {
     "bnf_cg_solve": [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_int)],
     "bnf_yee_points": [_P, C.c_int, C.c_int, C.POINTER(C.c_double)],
     "bnf_solver_create": [_P, C.POINTER(Opts), C.POINTER(_P)],
+    "bnf_nccl_unique_id": [C.c_char_p],
+    "bnf_solver_create_dist": [_P, C.POINTER(Opts), C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)],
     "bnf_set_epsilon": [_P, _P, C.c_int],
     "bnf_set_kappa": [_P, C.POINTER(C.c_double)],
     "bnf_apply_Ar": [_P, _P, _P, C.c_int, C.c_int],
@@ -94,6 +96,7 @@ _lib.bnf_opts_default.restype = None
 FRAME_SNAPPED, FRAME_ORIGINAL = 0, 1
 
 EXPORTS = ["bnf_lattice_create", "bnf_lattice_query", "bnf_lattice_destroy", "bnf_kvec_reduce",
+           "bnf_nccl_unique_id", "bnf_solver_create_dist",
            "bnf_kappa_canonical", "bnf_cg_solve", "bnf_yee_points",
            "bnf_opts_default", "bnf_solver_create", "bnf_solver_destroy", "bnf_set_epsilon", "bnf_set_kappa",
            "bnf_apply_Ar", "bnf_solve", "bnf_eigvecs", "bnf_kernel_times", "bnf_kernel_times_reset", "bnf_set_profile", "bnf_phase_counters",
@@ -164,8 +167,16 @@ class Lattice:
             self._h = None
 
 
+def nccl_unique_id():
+    """NCCL unique id (128 bytes) for bnf_solver_create_dist; broadcast it to every rank."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.bnf_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Solver:
-    def __init__(self, lattice: Lattice, device=0, stream=None, **kw):
+    def __init__(self, lattice: Lattice, device=0, stream=None, dist=None, **kw):
+        """dist = (nranks, rank, nccl_id): distributed slab mode (bnf_solver_create_dist)."""
         o = Opts()
         _lib.bnf_opts_default(C.byref(o))
         o.device = int(device)
@@ -173,7 +184,11 @@ class Solver:
         for k, v in kw.items():
             setattr(o, k, v)
         h = _P()
-        _check(_lib.bnf_solver_create(lattice._h, C.byref(o), C.byref(h)))
+        if dist is not None:
+            nranks, rank, uid = dist
+            _check(_lib.bnf_solver_create_dist(lattice._h, C.byref(o), int(nranks), int(rank), bytes(uid), C.byref(h)))
+        else:
+            _check(_lib.bnf_solver_create(lattice._h, C.byref(o), C.byref(h)))
         self._h = h
         self.lattice = lattice
         self.n = lattice.nn

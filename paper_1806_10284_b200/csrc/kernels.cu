@@ -1060,18 +1060,20 @@ __global__ void __launch_bounds__(1024) k_cg_finish(CGFuse cg, int which, int nv
         const int vl = warp / wpv, wi = warp % wpv;
         double acc = 0.0;
         if (vl < nv) {
-            const double* pp = part + (size_t)(v0 + vl) * nb;
             const int st = wpv * 32;
-            int t = wi * 32 + lane;
-            for (; t + 3 * st < nb; t += 4 * st) {
-                const double a0 = __ldcg(pp + t), a1 = __ldcg(pp + t + st);
-                const double a2 = __ldcg(pp + t + 2 * st), a3 = __ldcg(pp + t + 3 * st);
-                acc += a0;
-                acc += a1;
-                acc += a2;
-                acc += a3;
+            for (int sl = 0; sl < max(1, cg.nslab); ++sl) {   // slab-major partials [slab][vec][nb]
+                const double* pp = part + ((size_t)sl * nvec + v0 + vl) * nb;
+                int t = wi * 32 + lane;
+                for (; t + 3 * st < nb; t += 4 * st) {
+                    const double a0 = __ldcg(pp + t), a1 = __ldcg(pp + t + st);
+                    const double a2 = __ldcg(pp + t + 2 * st), a3 = __ldcg(pp + t + 3 * st);
+                    acc += a0;
+                    acc += a1;
+                    acc += a2;
+                    acc += a3;
+                }
+                for (; t < nb; t += st) acc += __ldcg(pp + t);
             }
-            for (; t < nb; t += st) acc += __ldcg(pp + t);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

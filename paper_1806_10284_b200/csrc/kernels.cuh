@@ -1,6 +1,7 @@
 // Device-side parameter blocks and kernel launchers (internal).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -67,6 +68,7 @@ struct OpArgs {
     long long vsf;              // Fourier-side vector stride (elements): 2 nloc, or 2n for virtual slabs
     long long nblk;             // n1 n2loc n3loc: one (slab pair, vector, component) exchange block
     int zcfg;                   // z-pass variant: bit 0 = stage x / r tiles with the inputs (CG), bit 1 = half-width tiles
+    int plane_t;                // plane pass staged by TMA (plane_tma.cu)
 };
 
 struct Profiler;  // host-side, see solver.cu
@@ -89,6 +91,7 @@ struct CGFuse {
     int* nb_z;                         //   (reduced by k_cg_finish after the pass)
     int* iter;                         // CG iterations done (device), or null
     int max_iter;
+    int nslab;                         // partial blocks per vector: [slab][vec][nb] (slab decomposition), 1
     int use_cond;                      // 1: set the CG graph's while-condition
     cudaGraphConditionalHandle cond;
 };
@@ -118,12 +121,19 @@ size_t cg_partials_per_vec(const OpArgs& a);
 // component slabs, one HBM read + write.  Square xy planes with a fast plan.
 bool plane_supported(const OpArgs& a);
 bool plane_w_supported(const OpArgs& a);
+// TMA-staged plane pass (plane_tma.cu): one slab, square 64/128/256 planes.  The
+// tensor maps describe the plane buffer as [planes][N][2N doubles] (plane_t_encode).
+bool plane_t_supported(const OpArgs& a);
+int plane_t_encode(const OpArgs& a, void* base, long long planes, void* encode_fn, CUtensorMap* my, CUtensorMap* mx);
+cudaError_t launch_plane_tma(const OpArgs& a, int nslab, const CGFuse* cg, cudaStream_t st, const CUtensorMap& my,
+                             const CUtensorMap& mx, int zbase);
 
 // Persistent, cp.async-pipelined z passes (zpass.cu).  cg == nullptr: plain
 // op (0 = A_r, 1 = M); otherwise the CG-fused variants (x update deferred:
 // zfwd2 does x += alpha_prev p, p <- r + beta p; zadj2 does r -= alpha M p and
 // the (r,r)/beta reduction; finish with launch_cg_xfinal).
 bool zpass2_supported(const OpArgs& a);
+int zpass2_tiles_x(const OpArgs& a);
 cudaError_t launch_zfwd2(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, double2* P, double2* X,
                          const CGFuse* cg, cudaStream_t st);
 cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nvec, int op, const CGFuse* cg,

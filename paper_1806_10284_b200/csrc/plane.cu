@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         // per-CTA partials of (p, M p) for every vector
         const int nvec = nslab / 3;
         const int nb = gridDim.x;
-        if (tid < nvec) cgf.part_x[((size_t)tid * a.nslab + a.slab) * nb + blockIdx.x] = acc_s[tid];
+        if (tid < nvec) cgf.part_x[(size_t)tid * nb + blockIdx.x] = acc_s[tid];
         __syncthreads();
-        if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb * a.nslab;   // alpha: k_cg_finish after this pass
+        if (blockIdx.x == 0 && tid == 0) *cgf.nb_x = nb;   // alpha: k_cg_finish after this pass
     }
 }
 
@@ -397,9 +397,9 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         // this plane's (p, M p) partial; alpha is formed by k_cg_finish after this pass
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        cg_block_partial(pmp, cgf.part_x + ((size_t)vec * (SL ? a.nslab : 1) + (SL ? a.slab : 0)) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        cg_block_partial(pmp, cgf.part_x + ((size_t)(SL ? a.slab * (gridDim.y / 3) : 0) + vec) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (lin == 0 && tid == 0) *cgf.nb_x = SL ? nb * a.nslab : nb;
+        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
     }
 }
 
@@ -542,9 +542,9 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_plane_w(double2* __restrict__
     if (CG) {
         const int vec = vl / 3;
         const int nb = gridDim.x * 3;
-        cg_block_partial(pmp, cgf.part_x + ((size_t)vec * (SL ? a.nslab : 1) + (SL ? a.slab : 0)) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
+        cg_block_partial(pmp, cgf.part_x + ((size_t)(SL ? a.slab * (gridDim.y / 3) : 0) + vec) * nb + (size_t)l * gridDim.x + blockIdx.x, D);
         const long long lin = (long long)vl * gridDim.x + blockIdx.x;
-        if (lin == 0 && tid == 0) *cgf.nb_x = SL ? nb * a.nslab : nb;
+        if (lin == 0 && tid == 0) *cgf.nb_x = nb;
     }
 }
 

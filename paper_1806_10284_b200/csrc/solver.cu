@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -242,6 +244,45 @@ struct GrowBuf {
     }
 };
 
+// NCCL, loaded at run time (dlopen) so that the library has no link-time
+// NCCL dependency: the process's already-loaded libnccl.so.2 (e.g. torch's)
+// is reused, else the system one.  Distributed slab mode only.
+struct Nccl {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclGetErrorString) errStr = nullptr;
+    bool ok = false;
+    static const Nccl& get() {
+        static Nccl x = [] {
+            Nccl n;
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+            if (!h) h = dlopen(std::getenv("BNF_NCCL_LIB") ? std::getenv("BNF_NCCL_LIB") : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) return n;
+            n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+            n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+            n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+            n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
+            n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
+            n.send = (decltype(n.send))dlsym(h, "ncclSend");
+            n.recv = (decltype(n.recv))dlsym(h, "ncclRecv");
+            n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
+            n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+            n.errStr = (decltype(n.errStr))dlsym(h, "ncclGetErrorString");
+            n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.groupStart && n.groupEnd && n.send && n.recv &&
+                   n.allReduce && n.allGather && n.errStr;
+            return n;
+        }();
+        return x;
+    }
+};
+
 }  // namespace
 
 // ------------------------------------------------------------- profiler
@@ -350,13 +391,22 @@ struct bnf_solver {
     double2* h_small = nullptr;  // pinned scratch for small matrices
     size_t h_small_cap = 0;
     int nblk = 592;
-    int nsl = 1;              // virtual slabs on this device (opts.slabs)
+    int nsl = 1;              // slabs of the decomposition (opts.slabs, or the ranks of bnf_solver_create_dist)
+    bool dist = false;        // one slab per process (NCCL), this process = slab `rank`
+    int rank = 0;
+    ncclComm_t comm = nullptr;
+    long long nv = 0;         // half-length of a vector held by this process (n, or n / nsl when dist)
+    bool plane_t_ok = false;  // TMA plane pass available (square 64/128/256 planes, one slab)
+    alignas(64) CUtensorMap tm_y, tm_x;   // TMA maps of U (plane_tma.cu), valid for (tm_base, tm_planes)
+    void* tm_base = nullptr;
+    long long tm_planes = 0;
     DevBuf Ub;                // plane-side buffer of the slab exchange (3n per vector)
     Profiler prof;
     long long matvecs = 0;
     long long inner_iters = 0;
 
     ~bnf_solver() {
+        if (comm) Nccl::get().commDestroy(comm);
         for (auto& c : cgg)
             if (c.exec) cudaGraphExecDestroy(c.exec);
         if (cap) cudaStreamDestroy(cap);
@@ -413,8 +463,8 @@ int ensure_small_host(bnf_solver* s, size_t count) {
 
 // ------------------------------------------------------------- operator
 int ensure_work(bnf_solver* s, int nvec) {
-    CK(s->U.ensure((size_t)3 * s->n * nvec * sizeof(double2)));
-    if (s->nsl > 1) CK(s->Ub.ensure((size_t)3 * s->n * nvec * sizeof(double2)));
+    CK(s->U.ensure((size_t)3 * s->nv * nvec * sizeof(double2)));
+    if (s->nsl > 1 || s->dist) CK(s->Ub.ensure((size_t)3 * s->nv * nvec * sizeof(double2)));
     return BNF_OK;
 }
 
@@ -434,10 +484,54 @@ OpArgs slab_args(const bnf_solver* s, int r) {
     a.j0 = r * a.n2loc;
     a.nloc = s->n / P;
     a.nblk = a.nloc / P;
-    a.vsf = 2 * s->n;
-    if (a.eps_idx) a.eps_idx += (size_t)r * 3 * a.nloc;
-    if (a.eps_inv) a.eps_inv += (size_t)r * 3 * a.nloc;
+    a.vsf = 2 * s->nv;
+    if (!s->dist) {   // virtual: every slab's eps on this device, slab-major
+        if (a.eps_idx) a.eps_idx += (size_t)r * 3 * a.nloc;
+        if (a.eps_inv) a.eps_inv += (size_t)r * 3 * a.nloc;
+    }
     return a;
+}
+
+long long sig_nloc(const bnf_solver* s) { return s->dist ? s->nv : s->n / s->nsl; }
+
+#define NCK(call)                                                                                   \
+    do {                                                                                            \
+        ncclResult_t _r = (call);                                                                   \
+        if (_r != ncclSuccess) {                                                                    \
+            set_error(std::string("NCCL: ") + Nccl::get().errStr(_r) + " at " + #call);           \
+            return BNF_ENCCL;                                                                       \
+        }                                                                                           \
+    } while (0)
+
+// Distributed slab mode: the all-to-all of the slab decomposition between the
+// ranks (one NCCL group of sends / receives; fwd: this rank's U block q -> rank
+// q's plane buffer block `rank`; back: the reverse).  Blocks of nvec 3 nblk.
+int nccl_exchange(bnf_solver* s, double2* U, double2* Ub, int nvec, int fwd) {
+    const Nccl& nc = Nccl::get();
+    const int P = s->nsl;
+    const size_t blk = (size_t)nvec * 3 * (size_t)(s->n / P / P);
+    NCK(nc.groupStart());
+    for (int q = 0; q < P; ++q) {
+        NCK(nc.send(fwd ? (const void*)(U + q * blk) : (const void*)(Ub + q * blk), 2 * blk, ncclFloat64, q, s->comm, s->st));
+        NCK(nc.recv(fwd ? (void*)(Ub + q * blk) : (void*)(U + q * blk), 2 * blk, ncclFloat64, q, s->comm, s->st));
+    }
+    NCK(nc.groupEnd());
+    return BNF_OK;
+}
+
+// element-wise sum over the ranks of count doubles (in place); no-op unless dist
+int nccl_sum(bnf_solver* s, double* x, size_t count) {
+    if (!s->dist) return BNF_OK;
+    NCK(Nccl::get().allReduce(x, x, count, ncclFloat64, ncclSum, s->comm, s->st));
+    return BNF_OK;
+}
+
+// CG partials [slab][vec][nb]: gather every rank's block (in place); no-op unless dist
+int nccl_gather_partials(bnf_solver* s, double* part, int nvec, int nb) {
+    if (!s->dist) return BNF_OK;
+    const size_t cnt = (size_t)nvec * nb;
+    NCK(Nccl::get().allGather(part + (size_t)s->rank * cnt, part, cnt, ncclFloat64, s->comm, s->st));
+    return BNF_OK;
 }
 
 // The all-to-all of the slab decomposition as device copies: plane-side slab q
@@ -457,15 +551,56 @@ cudaError_t slab_exchange(bnf_solver* s, double2* U, double2* Ub, int nvec, int 
 }
 
 const char* plane_name(const OpArgs& a, bool cg) {
+    if (a.plane_t) return cg ? "plane_t_cg" : "plane_t";
     if (a.plane_w) return a.plane_w == 2 ? (cg ? "plane_ws_cg" : "plane_ws") : (cg ? "plane_w_cg" : "plane_w");
     if (a.plane_l2) return cg ? "plane_l2_cg" : "plane_l2";
     return cg ? "plane_cg" : "plane";
+}
+
+void* tensor_map_encoder() {
+    static void* fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return f;
+    }();
+    return fn;
+}
+
+// the real-space middle on U (one slab): TMA plane pass, or plane.cu's variants
+cudaError_t run_plane(bnf_solver* s, const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
+    if (a.plane_t) {
+        const long long plane = (long long)a.mp.n1 * a.mp.n2;
+        const long long planes = (long long)(s->U.bytes / sizeof(double2)) / plane;
+        if (s->tm_base != s->U.p || s->tm_planes != planes) {
+            if (!tensor_map_encoder() || plane_t_encode(a, s->U.p, planes, tensor_map_encoder(), &s->tm_y, &s->tm_x) != 0)
+                return cudaErrorInvalidValue;
+            s->tm_base = s->U.p;
+            s->tm_planes = planes;
+        }
+        const int zbase = (int)((U - s->U.as<double2>()) / plane);
+        return launch_plane_tma(a, nslab, cg, st, s->tm_y, s->tm_x, zbase);
+    }
+    return launch_plane(a, U, nslab, cg, st);
 }
 
 // out = op(y) for nvec vectors (device pointers, 2n each)
 int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     TRY(ensure_work(s, nvec));
     double2* U = s->U.as<double2>();
+    if (s->dist) {   // one slab per process: z pass on this j-slab, NCCL all-to-all, plane on this z-slab, back
+        const OpArgs a = slab_args(s, s->rank);
+        double2* Ub = s->Ub.as<double2>();
+        RUN("zfwd2", launch_zfwd2(a, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
+        TRY(nccl_exchange(s, U, Ub, nvec, 1));
+        RUN(plane_name(a, false), launch_plane(a, Ub, 3 * nvec, nullptr, s->st));
+        TRY(nccl_exchange(s, U, Ub, nvec, 0));
+        RUN("zadj2", launch_zadj2(a, U, out, nvec, op, nullptr, s->st));
+        s->matvecs += nvec;
+        return BNF_OK;
+    }
     if (s->nsl > 1) {   // virtual slabs: z pass per j-slab, exchange, plane per z-slab, exchange, adjoint z pass
         const int P = s->nsl;
         const size_t nloc = (size_t)(s->n / P), part = (size_t)nvec * 3 * nloc;
@@ -485,7 +620,7 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     if (s->use_z2) RUN("zfwd2", launch_zfwd2(s->args, y, U, nvec, op, nullptr, nullptr, nullptr, s->st));
     else RUN("zfwd", launch_zfwd(s->args, y, U, nvec, op, s->st));
     if (s->use_plane) {
-        RUN(plane_name(s->args, false), launch_plane(s->args, U, 3 * nvec, nullptr, s->st));
+        RUN(plane_name(s->args, false), run_plane(s, s->args, U, 3 * nvec, nullptr, s->st));
     } else {
         RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
@@ -503,37 +638,50 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
 int autotune_plane(bnf_solver* s, int nvec) {
     if (s->plane_tuned || !s->plane_ok) return BNF_OK;
     s->plane_tuned = true;
-    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE") || std::getenv("BNF_PLANE_W")) {
+    if (s->dist) {   // every rank must run the same passes: no per-rank timing; L2 plane (or warp-local if forced)
+        s->use_plane = true;
+        s->args.plane_t = 0;
+        s->args.plane_w = std::getenv("BNF_PLANE_W") ? std::atoi(std::getenv("BNF_PLANE_W")) : 0;
+        s->args.plane_l2 = s->args.plane_w ? 0 : 1;
+        s->kver++;
+        return BNF_OK;
+    }
+    if (std::getenv("BNF_NO_PLANE") || std::getenv("BNF_PLANE") || std::getenv("BNF_PLANE_W") ||
+        std::getenv("BNF_PLANE_T")) {
         s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? std::atoi(std::getenv("BNF_PLANE_L2")) : 0;
         s->args.plane_w = std::getenv("BNF_PLANE_W") ? std::atoi(std::getenv("BNF_PLANE_W")) : 0;
-        if (std::getenv("BNF_NO_PLANE")) s->args.plane_w = 0;
+        s->args.plane_t = (std::getenv("BNF_PLANE_T") && s->plane_t_ok) ? 1 : 0;
+        if (std::getenv("BNF_NO_PLANE")) s->args.plane_w = s->args.plane_t = 0;
         s->use_plane = std::getenv("BNF_NO_PLANE") == nullptr;
         s->kver++;
         return BNF_OK;
     }
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     DevBuf y, o;
     CK(y.ensure((size_t)N * nvec * sizeof(double2)));
     CK(o.ensure((size_t)N * nvec * sizeof(double2)));
     CK(cudaMemsetAsync(y.p, 0, (size_t)N * nvec * sizeof(double2), s->st));
-    RUN("fill_random", launch_fill_random(y.as<double2>(), N, nvec, 12345ull, 0, nullptr, s->n, s->st));
+    RUN("fill_random", launch_fill_random(y.as<double2>(), N, nvec, 12345ull, 0, nullptr, s->nv, s->st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2,
-    // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles)
-    const int nvar = plane_w_supported(s->args) ? 5 : 3;
+    // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles),
+    // 5 = plane via L2 staged by TMA
+    const int nvar = s->plane_t_ok ? 6 : plane_w_supported(s->args) ? 5 : 3;
     const int v0 = s->nsl > 1 ? 2 : 0;   // slab mode: plane passes through L2 only (slab-aware)
-    float best[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    float best[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;
     auto set = [&](int variant) {
         s->use_plane = variant >= 1;
         s->args.plane_l2 = variant == 2 ? 1 : 0;
-        s->args.plane_w = variant >= 3 ? variant - 2 : 0;
+        s->args.plane_w = (variant == 3 || variant == 4) ? variant - 2 : 0;
+        s->args.plane_t = variant == 5 ? 1 : 0;
     };
     for (int variant = v0; variant < nvar; ++variant) {
+        if (s->nsl > 1 && variant == 5) continue;   // TMA plane: one slab only
         set(variant);
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
         CK(cudaEventRecord(e0, s->st));
@@ -544,7 +692,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
     }
     int pick = v0;
     for (int variant = v0 + 1; variant < nvar; ++variant)
-        if (best[variant] < best[pick]) pick = variant;
+        if (best[variant] > 0.f && best[variant] < best[pick]) pick = variant;
     set(pick);
     s->matvecs = mv0;
     s->prof.on = prof;
@@ -559,6 +707,7 @@ int dots(bnf_solver* s, const double2* X, const double2* Y, long long N, int nve
     double2* part = s->partial.as<double2>();
     RUN("dot", launch_dot_partial(X, Y, N, nvec, part, s->nblk, s->st));
     RUN("dot_final", launch_dot_final(part, s->nblk, nvec, out, s->st));
+    TRY(nccl_sum(s, reinterpret_cast<double*>(out), 2 * (size_t)nvec));   // distributed vectors: sum over ranks
     return BNF_OK;
 }
 
@@ -577,7 +726,7 @@ int gemm_tn(bnf_solver* s, const double2* X, int p, const double2* Y, int q, lon
 // Solve M X = C for nvec right-hand sides: plain CG, no
 // preconditioner, per-column stopping ||r|| <= tol ||c||.
 int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     const size_t vb = (size_t)N * nvec * sizeof(double2);
     CK(s->cgr.ensure(vb));
     CK(s->cgp.ensure(vb));
@@ -626,6 +775,22 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
         if (e != cudaSuccess) return e;   \
         ++k;                              \
     } while (0)
+    if (s->dist) {   // one slab per process: NCCL all-to-alls, CG partials all-gathered across the ranks
+        const OpArgs a = slab_args(s, s->rank);
+        double2* Ub = s->Ub.as<double2>();
+        auto ck = [&](int rc) { return rc == BNF_OK ? cudaSuccess : cudaErrorUnknown; };
+        BNF_K(launch_zfwd2(a, R, U, nvec, 1, P, X, &cg, st));
+        BNF_K(ck(nccl_exchange(s, U, Ub, nvec, 1)));
+        BNF_K(launch_plane(a, Ub, 3 * nvec, &cg, st));
+        BNF_K(ck(nccl_gather_partials(s, cg.part_x, nvec, 3 * a.n3loc)));
+        BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        BNF_K(ck(nccl_exchange(s, U, Ub, nvec, 0)));
+        BNF_K(launch_zadj2(a, U, R, nvec, 1, &cg, st));
+        BNF_K(ck(nccl_gather_partials(s, cg.part_z, nvec, zpass2_tiles_x(a) * a.n2loc)));
+        BNF_K(launch_cg_finish(cg, 1, nvec, st));
+        *nk = k;
+        return cudaSuccess;
+    }
     if (s->nsl > 1) {   // virtual slabs: per-slab passes, device-copy all-to-alls
         const int NS = s->nsl;
         const size_t nloc = (size_t)(s->n / NS), part = (size_t)nvec * 3 * nloc;
@@ -646,7 +811,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     if (s->use_z2) BNF_K(launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, st));
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
-        BNF_K(launch_plane(s->args, U, 3 * nvec, &cg, st));
+        BNF_K(run_plane(s, s->args, U, 3 * nvec, &cg, st));
         BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
@@ -726,7 +891,7 @@ int cg_graph(bnf_solver* s, const CGFuse& cg0, double2* R, double2* P, double2* 
 // has a register-FFT plan.  Without profiling the loop runs as one CUDA
 // graph with a device-side while condition.
 int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     const size_t vb = (size_t)N * nvec * sizeof(double2);
     CK(s->cgr.ensure(vb));
     CK(s->cgp.ensure(vb));
@@ -764,7 +929,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
         cg.iter = nullptr;
         for (; it < s->o.max_inner; ++it) {
             // eager: one timed launch per pass (profiling, bnf_kernel_times)
-            if (s->nsl > 1) {
+            if (s->nsl > 1 || s->dist) {
                 int nk = 0;
                 RUN("cg_iter_slabs", cg_iter_kernels(s, cg, R, P, U, X, nvec, s->st, &nk));
                 s->prof.launches += nk - 1;
@@ -772,7 +937,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             if (s->use_z2) RUN("zfwd2_cg", launch_zfwd2(s->args, R, U, nvec, 1, P, X, &cg, s->st));
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
-                RUN(plane_name(s->args, true), launch_plane(s->args, U, 3 * nvec, &cg, s->st));
+                RUN(plane_name(s->args, true), run_plane(s, s->args, U, 3 * nvec, &cg, s->st));
                 RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
@@ -804,13 +969,13 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
 
 // Y = Sigma^{-1} CG(M, Sigma^{-1} X)  =  A_r^{-1} X
 int apply_Ar_inv(bnf_solver* s, const double2* X, double2* Y, int nvec) {
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     CK(s->cgc.ensure((size_t)N * nvec * sizeof(double2)));
     double2* C = s->cgc.as<double2>();
-    RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->n, nvec, 1, s->st, s->n / s->nsl));
+    RUN("scale_sigma", launch_scale_sigma(X, C, s->sigma.as<double>(), s->nv, nvec, 1, s->st, sig_nloc(s)));
     if (s->fused_ok) TRY(cg_solve_fused(s, C, Y, nvec, nullptr));
     else TRY(cg_solve(s, C, Y, nvec, nullptr));
-    RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->n, nvec, 1, s->st, s->n / s->nsl));
+    RUN("scale_sigma", launch_scale_sigma(Y, Y, s->sigma.as<double>(), s->nv, nvec, 1, s->st, sig_nloc(s)));
     return BNF_OK;
 }
 
@@ -834,13 +999,14 @@ int put_small(bnf_solver* s, const std::vector<cd>& in, double2* dev) {
 
 // H = X^* Y for q possibly > 8 (column chunks); host result p x q row-major
 int gram_host(bnf_solver* s, const double2* X, int p, const double2* Y, int q, std::vector<cd>& H) {
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     H.assign((size_t)p * q, 0.0);
     double2* Hd = s->small.as<double2>() + 64;
     std::vector<cd> tmp;
     for (int c0 = 0; c0 < q; c0 += 8) {
         const int qc = std::min(8, q - c0);
         TRY(gemm_tn(s, X, p, Y + (size_t)c0 * N, qc, N, Hd));
+        TRY(nccl_sum(s, reinterpret_cast<double*>(Hd), 2 * (size_t)p * qc));   // distributed vectors: sum over ranks
         TRY(get_small(s, Hd, p * qc, tmp));
         for (int a = 0; a < p; ++a)
             for (int c = 0; c < qc; ++c) H[(size_t)a * q + c0 + c] = tmp[(size_t)a * qc + c];
@@ -851,7 +1017,7 @@ int gram_host(bnf_solver* s, const double2* X, int p, const double2* Y, int q, s
 // Y[:, c] = beta Y[:, c] + alpha X H[:, c]  (H host p x q row-major; column chunks of 8)
 int gemm_nn_host(bnf_solver* s, const double2* X, int p, const std::vector<cd>& H, int q, double2* Y, double alpha,
                  double beta) {
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     double2* Hd = s->small.as<double2>() + 64;
     for (int c0 = 0; c0 < q; c0 += 8) {
         const int qc = std::min(8, q - c0);
@@ -883,7 +1049,7 @@ int chol_qr2(bnf_solver* s, double2* W, int q, std::vector<cd>& Rtot, bool& ok) 
         if (q <= 8) {
             TRY(gemm_nn_host(s, W, q, Ri, q, W, 1.0, 0.0));  // in place is safe for one column chunk
         } else {
-            const long long N = 2 * s->n;
+            const long long N = 2 * s->nv;
             CK(s->cgc.ensure((size_t)N * q * sizeof(double2)));
             TRY(gemm_nn_host(s, W, q, Ri, q, s->cgc.as<double2>(), 1.0, 0.0));
             RUN("copy", launch_copy(W, s->cgc.as<double2>(), N * q, s->st));
@@ -943,7 +1109,11 @@ int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
         }
         p.gamma = i0 + (long long)n1 * (j0 + (long long)n2 * k0);
     }
-    RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st, 0, s->L.n[1] / s->nsl, s->n));
+    if (s->dist)   // this rank's j-slab
+        RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st, s->rank * (s->L.n[1] / s->nsl),
+                                              s->L.n[1] / s->nsl, s->nv));
+    else
+        RUN("sigma_table", launch_sigma_table(p, s->sigma.as<double>(), s->st, 0, s->L.n[1] / s->nsl, s->n));
     s->kappa_set = true;
     s->kver++;
     return BNF_OK;
@@ -1115,6 +1285,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     const Lattice& L = s->L;
     const int n1 = L.n[0], n2 = L.n[1], n3 = L.n[2];
     s->n = (long long)n1 * n2 * n3;
+    s->nv = s->n;
     const long long n = s->n;
     // axis plans + root tables
     AxisPlan* plans[3] = {&s->args.px, &s->args.py, &s->args.pz};
@@ -1225,6 +1396,8 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->use_z2 = s->fused_ok && zpass2_supported(s->args) && std::getenv("BNF_NO_Z2") == nullptr;
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
+    s->plane_t_ok = s->use_z2 && plane_t_supported(s->args) && tensor_map_encoder() != nullptr &&
+                    std::getenv("BNF_NO_PLANE_T") == nullptr;
     // virtual slabs (SURVEY §8(e) / DESIGN §8): the slab-decomposed operator with the
     // all-to-alls as device copies; needs the fast z passes and an L2 plane middle
     s->nsl = std::max(1, o.slabs);
@@ -1259,8 +1432,56 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         s->cgf.beta = s->cgs.beta;
         s->cgf.thr = s->cgs.thr;
         s->cgf.active = s->cgs.active;
+        s->cgf.nslab = s->nsl;
     }
     *out = s.release();
+    return BNF_OK;
+}
+
+int bnf_nccl_unique_id(unsigned char id[128]) {
+    if (!id) {
+        set_error("NULL argument");
+        return BNF_EINVAL;
+    }
+    const Nccl& nc = Nccl::get();
+    if (!nc.ok) {
+        set_error("libnccl.so.2 could not be loaded (set BNF_NCCL_LIB)");
+        return BNF_ENCCL;
+    }
+    ncclUniqueId u;
+    NCK(nc.getUniqueId(&u));
+    std::memcpy(id, u.internal, 128);
+    return BNF_OK;
+}
+
+int bnf_solver_create_dist(const bnf_lattice* lat, const bnf_opts* opts, int nranks, int rank, const unsigned char id[128],
+                           bnf_solver** out) {
+    if (!lat || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("invalid argument");
+        return BNF_EINVAL;
+    }
+    const Nccl& nc = Nccl::get();
+    if (!nc.ok) {
+        set_error("libnccl.so.2 could not be loaded (set BNF_NCCL_LIB)");
+        return BNF_ENCCL;
+    }
+    bnf_opts o;
+    bnf_opts_default(&o);
+    if (opts) o = *opts;
+    o.slabs = nranks;   // the slab geometry of the decomposition (validated by bnf_solver_create)
+    bnf_solver* s = nullptr;
+    TRY(bnf_solver_create(lat, &o, &s));
+    std::unique_ptr<bnf_solver> g(s);
+    s->dist = true;
+    s->rank = rank;
+    s->nv = s->n / nranks;
+    s->use_graph = false;   // NCCL calls inside the CG loop: eager loop with a host convergence check
+    s->cgf.nslab = nranks;
+    s->args.plane_t = 0;
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    NCK(nc.commInitRank(&s->comm, nranks, u, rank));
+    *out = g.release();
     return BNF_OK;
 }
 
@@ -1323,7 +1544,20 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
         }
         idx[t] = (unsigned char)lastk;
     }
-    if (s->nsl > 1) {   // slab-major [slab][l][cl][b][a] (real-space z-slabs of n3 / P planes)
+    if (s->dist) {   // this rank's real-space z-slab [l][cl][b][a]
+        const int P = s->nsl;
+        const long long plane = (long long)s->L.n[0] * s->L.n[1], n = s->n, nloc = n / P, n3l = s->L.n[2] / P;
+        std::vector<double> h2(3 * nloc);
+        std::vector<unsigned char> i2(small ? 3 * nloc : 0);
+        for (int l = 0; l < 3; ++l)
+            for (long long cl = 0; cl < n3l; ++cl) {
+                const long long src = l * n + (s->rank * n3l + cl) * plane, dst = l * nloc + cl * plane;
+                std::memcpy(h2.data() + dst, h.data() + src, plane * sizeof(double));
+                if (small) std::memcpy(i2.data() + dst, idx.data() + src, plane);
+            }
+        h.swap(h2);
+        if (small) idx.swap(i2);
+    } else if (s->nsl > 1) {   // slab-major [slab][l][cl][b][a] (real-space z-slabs of n3 / P planes)
         const int P = s->nsl;
         const long long plane = (long long)s->L.n[0] * s->L.n[1], n = s->n, nloc = n / P, n3l = s->L.n[2] / P;
         std::vector<double> h2(n3);
@@ -1338,14 +1572,14 @@ int bnf_set_epsilon(bnf_solver* s, const double* eps, int mem) {
         h.swap(h2);
         if (small) idx.swap(i2);
     }
-    CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), n3 * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->eps_inv.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s->st));
     s->args.eps_idx = nullptr;
     s->args.eps_lut = nullptr;
     if (small) {
         CK(s->eps_idx.ensure(n3));
         CK(s->eps_lut.ensure(256 * sizeof(double)));
         vals.resize(256, 0.0);
-        CK(cudaMemcpyAsync(s->eps_idx.p, idx.data(), n3, cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemcpyAsync(s->eps_idx.p, idx.data(), idx.size(), cudaMemcpyHostToDevice, s->st));
         CK(cudaMemcpyAsync(s->eps_lut.p, vals.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, s->st));
         s->args.eps_idx = s->eps_idx.as<unsigned char>();
         s->args.eps_lut = s->eps_lut.as<double>();
@@ -1431,10 +1665,10 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
     TRY(set_kappa_impl(s, kappa));
     TRY(autotune_plane(s, s->o.block));
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     const int b = s->o.block;
     const int want = nev + s->o.guard;
-    const long long dof = N - (s->args.mp.gamma >= 0 ? 2 : 0);
+    const long long dof = 2 * s->n - (s->args.mp.gamma >= 0 ? 2 : 0);   // global NFSEP dimension
     if (want > dof) {
         set_error("nev + guard exceeds the NFSEP dimension");
         return BNF_EINVAL;
@@ -1459,7 +1693,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     CK(s->small.ensure((size_t)(64 + 8 * std::max<long long>((long long)(maxsteps + 1) * b, want)) * sizeof(double2)));
     double2* V = s->V.as<double2>();
     // start block: seeded counter-based normals, Gamma mode masked (R6)
-    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, 0, s->sigma.as<double>(), s->n, s->st, s->n / s->nsl));
+    RUN("fill_random", launch_fill_random(V, N, b, s->o.seed, (long long)s->rank * N * b, s->sigma.as<double>(), s->nv, s->st, sig_nloc(s)));
     if (s->o.warm && s->prev_want > 0) {
         // Warm start (DESIGN R17): start block = fixed pseudo-random combinations of
         // the previous solve's Ritz vectors (neighbouring k on the path) plus 1e-3 of
@@ -1475,8 +1709,8 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
             x = cd(((double)(h >> 11) / 9007199254740992.0) - 0.5, 0.0);
         }
         TRY(gemm_nn_host(s, s->Yv.as<double2>(), pw, Wm, b, V, 1.0, 1e-3));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 1, s->st, s->n / s->nsl));
-        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->n, b, 0, s->st, s->n / s->nsl));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->nv, b, 1, s->st, sig_nloc(s)));
+        RUN("scale_sigma", launch_scale_sigma(V, V, s->sigma.as<double>(), s->nv, b, 0, s->st, sig_nloc(s)));
     }
     bool ok = true;
     std::vector<cd> R0;
@@ -1541,7 +1775,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         TRY(chol_qr2(s, W, b, Rn, ok));
         if (!ok) {  // invariant subspace / breakdown: continue with a fresh random block
             RUN("fill_random", launch_fill_random(W, N, b, s->o.seed + 7919ull * (step + 1), 0,
-                                                  s->sigma.as<double>(), s->n, s->st, s->n / s->nsl));
+                                                  s->sigma.as<double>(), s->nv, s->st, sig_nloc(s)));
             for (int pass = 0; pass < 2; ++pass) {
                 TRY(gram_host(s, V, p, W, b, H));
                 TRY(gemm_nn_host(s, V, p, H, b, W, -1.0, 1.0));
@@ -1718,7 +1952,7 @@ int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
         set_error("no eigenvectors: call bnf_solve first");
         return BNF_ESTATE;
     }
-    const long long N = 2 * s->n;
+    const long long N = 2 * s->nv;
     const cudaMemcpyKind dir = (mem == BNF_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (kind == BNF_VEC_Y) {
         CK(cudaMemcpyAsync(out, s->Yv.p, (size_t)N * nev * sizeof(double2), dir, s->st));

@@ -306,11 +306,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     }
     if (MODE == 1) {
         // per-CTA partial of (r, r); beta is formed by k_cg_finish after this pass
-        // partials of every slab of a vector are contiguous: [vec][slab][block]
+        // partials slab-major [slab][vec][block] (k_cg_finish sums over slabs; all-gather in dist mode)
         const int nb = gridDim.x * gridDim.y;
-        cg_block_partial(rr, cg.part_z + ((size_t)vec * a.nslab + a.slab) * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x,
+        cg_block_partial(rr, cg.part_z + ((size_t)a.slab * gridDim.z + vec) * nb + (size_t)blockIdx.y * gridDim.x + blockIdx.x,
                          red);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb * a.nslab;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) *cg.nb_z = nb;
     }
 }
 
@@ -425,6 +425,23 @@ cudaError_t launch_zadj2(const OpArgs& a, const double2* U, double2* OUT, int nv
         BNF_Z2_PLANS(BNF_CASE)
 #undef BNF_CASE
         default: return cudaErrorNotSupported;
+    }
+}
+
+// CTAs per (j, vector) of the plan launch_zfwd2 / launch_zadj2 pick (= n1 / W):
+// the zadj CG pass writes (n1 / W) n2loc partials per vector and slab
+int zpass2_tiles_x(const OpArgs& a) {
+    if (a.zcfg & 2) switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: if (a.mp.n1 % WW == 0) return a.mp.n1 / WW; break;
+        BNF_Z2_HALF(BNF_CASE)
+#undef BNF_CASE
+        default: break;
+    }
+    switch (a.mp.n3) {
+#define BNF_CASE(NN, A, B, WW) case NN: return a.mp.n1 / WW;
+        BNF_Z2_PLANS(BNF_CASE)
+#undef BNF_CASE
+        default: return 0;
     }
 }
 

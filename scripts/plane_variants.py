@@ -22,7 +22,7 @@ from synthetic import configs  # noqa: E402
 
 VARIANTS = {"yxy": {"BNF_NO_PLANE": "1"}, "cluster": {"BNF_PLANE": "1"},
             "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"}, "warp_smem": {"BNF_PLANE_W": "1"},
-            "warp_shfl": {"BNF_PLANE_W": "2"}}
+            "warp_shfl": {"BNF_PLANE_W": "2"}, "tma": {"BNF_PLANE_T": "1"}}
 
 
 def main():
@@ -42,7 +42,7 @@ def main():
     c = torch.randn(args.b * 2 * n, dtype=torch.complex128, device="cuda", generator=g)
     ref = None
     for name in args.variants.split(","):
-        for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W"):
+        for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T"):
             os.environ.pop(k, None)
         os.environ.update(VARIANTS[name])
         st = torch.cuda.Stream()

@@ -472,11 +472,12 @@ def test_block_sizes_cg_solve(bnf, block):
 
 
 MIDDLES = {"cluster": {"BNF_PLANE": "1"}, "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"},
-           "yxy": {"BNF_NO_PLANE": "1"}, "warp_smem": {"BNF_PLANE_W": "1"}, "warp_shfl": {"BNF_PLANE_W": "2"}}
+           "yxy": {"BNF_NO_PLANE": "1"}, "warp_smem": {"BNF_PLANE_W": "1"}, "warp_shfl": {"BNF_PLANE_W": "2"},
+           "tma": {"BNF_PLANE_T": "1"}}
 
 
 def _forced_solver(bnf, monkeypatch, envs, cfg, n, **kw):
-    for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W"):
+    for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T"):
         monkeypatch.delenv(k, raising=False)
     for k, v in envs.items():
         monkeypatch.setenv(k, v)
@@ -624,3 +625,32 @@ def test_virtual_slabs_config5_golden(bnf, golden_dir, P):
     L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape, slabs=P)
     lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
     np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+
+
+def test_dist_single_rank_nccl(bnf):
+    """bnf_solver_create_dist with one rank: the NCCL path of the distributed
+    slab mode (send/recv all-to-all to itself, all-gathered CG partials,
+    all-reduced Gram products) runs for real and returns the whole-grid
+    operator (1e-13) and the oracle golden eigenvalues (1e-10), config 2 64^3."""
+    g = _golden(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"), "full_c2_k9_oracle.json")
+    cfg = configs.config(2)
+    n = tuple(g["n"])
+    L = bnf.Lattice(cfg.a_raw, n)
+    O = olat.snap(cfg.a_raw, n)
+    eps = E.sample(cfg.shape, n, O.a, O.delta, O.a_canon)
+    uid = bnf.nccl_unique_id()
+    S = bnf.Solver(L, dist=(1, 0, uid))
+    S.set_epsilon(E.stacked(eps))
+    S1 = bnf.Solver(L)
+    S1.set_epsilon(E.stacked(eps))
+    kap = tuple(g["kappa"])
+    y = vectors.complex_normal((2, 2 * O.nn), seed=41)
+    for code in (bnf.OP_AR, bnf.OP_M):
+        a = _apply_gpu(S, kap, y, code)
+        b = _apply_gpu(S1, kap, y, code)
+        assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+    lam, st = S.solve(kap, len(g["lambda"]))
+    assert st["converged"] == 1
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+    S.close()
+    S1.close()
