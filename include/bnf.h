@@ -69,6 +69,10 @@ extern "C" {
 #define BNF_VEC_Y 0     /* NFSEP eigenvectors y (2n complex each, unit 2-norm) */
 #define BNF_VEC_E 1     /* E-field eigenvectors e = B^{-1} Q_r Sigma_r y / sqrt(lambda) (3n complex,
                            e^* B e = 1), real-space Yee layout, Bloch phase included */
+#define BNF_VEC_H 2     /* H-field eigenvectors h = C e / (i omega) = -i P_r y (3n complex, h^* h = 1;
+                           C = P_r Sigma_r Q_r^*; Maxwell's curl equation):
+                           computed in the Fourier domain as -i T (lambda x (Pi1 y1 + Pi2 y2) / sigma) per
+                           mode, same real-space layout and Bloch phase as BNF_VEC_E; C^* h = -i omega B e */
 
 typedef struct bnf_lattice bnf_lattice;
 typedef struct bnf_solver bnf_solver;
@@ -229,8 +233,8 @@ int bnf_cg_solve(bnf_solver* s, const void* c, void* x, int b, int max_iter, int
    BNF_ENOCONV (with results) if the tolerance was not reached. */
 int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf_stats* stats);
 
-/* Eigenvectors of the last solve: kind = BNF_VEC_Y (out: nev x 2n complex)
-   or BNF_VEC_E (out: nev x 3n complex), mem = HOST or DEVICE. */
+/* Eigenvectors of the last solve: kind = BNF_VEC_Y (out: nev x 2n complex),
+   BNF_VEC_E or BNF_VEC_H (out: nev x 3n complex), mem = HOST or DEVICE. */
 int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem);
 
 /* Per-kernel device time (ms) accumulated since the last reset while

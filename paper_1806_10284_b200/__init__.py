@@ -22,7 +22,7 @@ _lib = C.CDLL(LIB_PATH)
 OK, EINVAL, EGEOM, ENOMEM, ECUDA, ENCCL, ENOCONV, ESTATE = range(8)
 MEM_HOST, MEM_DEVICE = 0, 1
 OP_AR, OP_M = 0, 1
-VEC_Y, VEC_E = 0, 1
+VEC_Y, VEC_E, VEC_H = 0, 1, 2
 
 
 class BnfError(RuntimeError):

@@ -288,8 +288,18 @@ __global__ void __launch_bounds__(256) k_zfwd(const double2* __restrict__ Y, dou
             double sig;
             mode_lambdas(p, i, j, kk, lam);
             mode_pis(p, lam, (long long)idx == p.gamma, pi1, pi2, sig);
-            const double s = (op == 0) ? sig : 1.0;
+            const double s = (op == 0) ? sig : (op == 2 ? (sig > 0.0 ? 1.0 / sig : 0.0) : 1.0);
             for (int l = 0; l < 3; ++l) o[l] = cscale(cadd(cmul(pi1[l], u1), cmul(pi2[l], u2)), s);
+            if (op == 2) {
+                // H side (NEXT-3): C (I x T) = (I x T) [lambda x], so
+                // H = C e / (i omega) = -i P_r y = -i (I x T) lambda x (Q-side combine of y / sigma)
+                const double2 h0 = csub(cmul(lam[1], o[2]), cmul(lam[2], o[1]));
+                const double2 h1 = csub(cmul(lam[2], o[0]), cmul(lam[0], o[2]));
+                const double2 h2 = csub(cmul(lam[0], o[1]), cmul(lam[1], o[0]));
+                o[0] = make_double2(h0.y, -h0.x);   // -i h
+                o[1] = make_double2(h1.y, -h1.x);
+                o[2] = make_double2(h2.y, -h2.x);
+            }
         }
         buf[0][e] = o[0];
         buf[1][e] = o[1];
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(256) k_xfwd_recover(double2* __restrict__ U, O
     const int b0 = blockIdx.x * R, c = blockIdx.y;
     const int vl = blockIdx.z, l = vl % 3, v = vl / 3;
     double2* Uv = U + (size_t)vl * n;
-    const double* einv = eps_inv + (size_t)l * n;
+    const double* einv = eps_inv ? eps_inv + (size_t)l * n : nullptr;   // null: no B^{-1} (H field)
     const size_t base = (size_t)n1 * ((size_t)b0 + (size_t)n2 * c);
     const int rows = min(R, n2 - b0);
     const int tile = n1 * ld;
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(256) k_xfwd_recover(double2* __restrict__ U, O
     const double sv = scale0 * (scales ? scales[v] : 1.0);
     for (int e = threadIdx.x; e < rows * n1; e += blockDim.x) {
         const int row = e / n1, aa = e - row * n1;
-        Uv[base + e] = cscale(res[aa * ld + row], sv * __ldg(einv + base + e));
+        Uv[base + e] = cscale(res[aa * ld + row], sv * (einv ? __ldg(einv + base + e) : 1.0));
     }
 }
 

@@ -1943,7 +1943,8 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
 }
 
 int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
-    if (!s || !out || (kind != BNF_VEC_Y && kind != BNF_VEC_E) || (mem != BNF_MEM_HOST && mem != BNF_MEM_DEVICE)) {
+    if (!s || !out || (kind != BNF_VEC_Y && kind != BNF_VEC_E && kind != BNF_VEC_H) ||
+        (mem != BNF_MEM_HOST && mem != BNF_MEM_DEVICE)) {
         set_error("invalid argument");
         return BNF_EINVAL;
     }
@@ -1959,10 +1960,11 @@ int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
         CK(cudaStreamSynchronize(s->st));
         return BNF_OK;
     }
-    if (s->nsl > 1) {
-        set_error("BNF_VEC_E is not available with opts.slabs > 1 (fetch BNF_VEC_Y, slab layout)");
+    if (s->nsl > 1 || s->dist) {
+        set_error("BNF_VEC_E / BNF_VEC_H are not available in slab mode (fetch BNF_VEC_Y, slab layout)");
         return BNF_EINVAL;
     }
+    const bool hfield = kind == BNF_VEC_H;
     // e = B^{-1} Q_r Sigma_r y / sqrt(lambda), Bloch phase of eq. (T) included
     const long long n = s->n;
     const size_t ebytes = (size_t)3 * n * sizeof(double2);
@@ -1977,10 +1979,11 @@ int bnf_eigvecs(bnf_solver* s, int kind, void* out, int mem) {
         TRY(ensure_work(s, qc));
         double2* U = s->U.as<double2>();
         const double2* Yc = s->Yv.as<double2>() + (size_t)c0 * N;
-        RUN("zfwd", launch_zfwd(s->args, Yc, U, qc, BNF_OP_AR, s->st));
+        RUN("zfwd", launch_zfwd(s->args, Yc, U, qc, hfield ? 2 : BNF_OP_AR, s->st));
         RUN("yfwd", launch_ypass(s->args, U, qc, 0, s->st));
-        RUN("xfwd_recover", launch_xfwd_recover(s->args, U, qc, s->eps_inv.as<double>(),
-                                                1.0 / std::sqrt((double)n), scales.as<double>() + c0, s->st));
+        RUN("xfwd_recover", launch_xfwd_recover(s->args, U, qc, hfield ? nullptr : s->eps_inv.as<double>(),
+                                                1.0 / std::sqrt((double)n), hfield ? nullptr : scales.as<double>() + c0,
+                                                s->st));
         RUN("bloch", launch_bloch_phase(s->args, U, qc, s->kappa[0], s->kh2, s->kh3, s->st));
         CK(cudaMemcpyAsync((char*)out + (size_t)c0 * ebytes, U, ebytes * qc, dir, s->st));
     }

@@ -654,3 +654,35 @@ def test_dist_single_rank_nccl(bnf):
     np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
     S.close()
     S1.close()
+
+
+def test_field_postprocessing_h_and_divergence(bnf):
+    """NEXT-3 field post-processing on config 1 (SC 12^3): the library's H
+    field (BNF_VEC_H, -i P_r y) and E field satisfy Maxwell's curl equations
+    with the oracle's independently assembled sparse Yee curl C:
+    C e = i omega h and C^* h = -i omega B e, h^* h = 1; and D = B e is
+    divergence-free, sum_l C_l^* D_l = 0 (Q0^* B e = 0)."""
+    cfg = configs.config(1)
+    L, O, eps, S = _setup(bnf, cfg.a_raw, cfg.n, cfg.shape)
+    kap = L.kvec_reduce(cfg.kpoints[0])
+    nev = 6
+    lam, st = S.solve(kap, nev)
+    Ef = np.zeros((nev, 3 * O.nn), dtype=np.complex128)
+    Hf = np.zeros((nev, 3 * O.nn), dtype=np.complex128)
+    S.eigvecs(bnf.VEC_E, Ef)
+    S.eigvecs(bnf.VEC_H, Hf)
+    C = curl.curl(O, kap)
+    C1, C2, C3 = curl.partials(O, kap)
+    Bd = curl.B_diag(eps)
+    n = O.nn
+    for i in range(nev):
+        w = math.sqrt(lam[i])
+        e, h = Ef[i], Hf[i]
+        np.testing.assert_allclose(np.vdot(h, h).real, 1.0, rtol=1e-9)
+        r1 = np.linalg.norm(C @ e - 1j * w * h) / (w * np.linalg.norm(h))
+        r2 = np.linalg.norm(C.conj().T @ h + 1j * w * Bd * e) / (w * np.linalg.norm(Bd * e))
+        assert r1 <= 1e-9 and r2 <= 1e-9, (i, r1, r2)
+        D = Bd * e
+        div = C1.conj().T @ D[:n] + C2.conj().T @ D[n:2 * n] + C3.conj().T @ D[2 * n:]
+        scale = max(np.linalg.norm(C1.conj().T @ D[:n]), 1e-300)
+        assert np.linalg.norm(div) <= 1e-10 * scale, (i, np.linalg.norm(div) / scale)
