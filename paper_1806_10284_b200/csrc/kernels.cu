@@ -17,6 +17,7 @@
 // All inter-axis twiddles have integer phase numerators (SURVEY §8 notation)
 // and are read from an exact two-level table of e^{2 pi i P/n}.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -584,6 +585,78 @@ __global__ void __launch_bounds__(256) k_gemm_tn_partial(const double2* __restri
     }
     __syncthreads();
     for (int t = threadIdx.x; t < p * q; t += blockDim.x) partial[(size_t)t * nblk + blockIdx.x] = acc[t];
+}
+
+// Tall-skinny X^* Y, register-accumulating variant: each warp owns up to CPW
+// columns of X (p >= 8: a = warp + 8 j) or, for p < 8, a column and a part of
+// every slice's rows (so that all 8 warps stream X); the partial dot products
+// stay in registers over the CTA's whole grid-stride range of 512-row slices
+// and are reduced (warp shuffles, then the row parts in a fixed order) once
+// at the end -- no per-slice reductions.  Y slices are staged in shared
+// memory (512-row slices; 256 for q > 4).  partial[(a*q + c)*nblk + blk], deterministic.
+template <int Q, int CPW>
+__global__ void __launch_bounds__(256) k_gemm_tn2(const double2* __restrict__ X, int p, const double2* __restrict__ Y,
+                                                  int q, long long N, double2* __restrict__ partial) {
+    constexpr int SL = Q >= 8 ? 256 : 512;   // rows per slice (static shared memory <= 48 KB)
+    __shared__ double2 ys[Q * SL];
+    __shared__ double2 red[8][Q];
+    const int nblk = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int parts = p >= 8 ? 1 : 8 / p;            // row parts per column (p < 8)
+    const int acol = p >= 8 ? warp : warp % p;        // first owned column
+    const int part = p >= 8 ? 0 : warp / p;
+    const bool active = part < parts;
+    const int r0 = part * (SL / parts), r1 = (part + 1) * (SL / parts);
+    double2 sum[CPW][Q];
+#pragma unroll
+    for (int j = 0; j < CPW; ++j)
+#pragma unroll
+        for (int c = 0; c < Q; ++c) sum[j][c] = make_double2(0, 0);
+    for (long long s0 = (long long)blockIdx.x * SL; s0 < N; s0 += (long long)gridDim.x * SL) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < Q * SL; t += blockDim.x) {
+            const int c = t / SL, r = t - c * SL;
+            ys[t] = (c < q && s0 + r < N) ? Y[(size_t)c * N + s0 + r] : make_double2(0, 0);
+        }
+        __syncthreads();
+        if (!active) continue;
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+            const int a = acol + 8 * j;
+            if (a >= p || (p < 8 && j > 0)) break;
+            const double2* xa = X + (size_t)a * N + s0;
+#pragma unroll 4
+            for (int r = r0 + lane; r < r1; r += 32) {
+                const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
+#pragma unroll
+                for (int c = 0; c < Q; ++c) sum[j][c] = cadd(sum[j][c], cjmul(x, ys[c * SL + r]));
+            }
+        }
+    }
+    // reduce: warp sums, then (p < 8) the row parts of a column in a fixed order
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+        const int a = acol + 8 * j;
+        const bool own = active && a < p && !(p < 8 && j > 0);
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+            const double2 v = warp_sum(sum[j][c]);
+            if (p >= 8) {
+                if (own && c < q && lane == 0) partial[(size_t)(a * q + c) * nblk + blockIdx.x] = v;
+            } else if (j == 0) {
+                if (lane == 0) red[warp][c] = v;
+            }
+        }
+    }
+    if (p < 8) {
+        __syncthreads();
+        if (threadIdx.x < p * q) {
+            const int a = threadIdx.x / q, c = threadIdx.x % q;
+            double2 acc = make_double2(0, 0);
+            for (int pt = 0; pt < parts; ++pt) acc = cadd(acc, red[a + pt * p][c]);
+            partial[(size_t)(a * q + c) * nblk + blockIdx.x] = acc;
+        }
+    }
 }
 
 // Y_c = beta Y_c + alpha sum_a X_a H[a*q + c]   (H on device, p*q <= 4096)
@@ -1297,6 +1370,26 @@ cudaError_t launch_dot_final(const double2* partial, int nblk, int nvec, double2
 
 cudaError_t launch_gemm_tn_partial(const double2* X, int p, const double2* Y, int q, long long N, double2* partial,
                                    int nblk, cudaStream_t st) {
+    static const bool v1 = std::getenv("BNF_GEMM_V1") != nullptr;
+    if (!v1 && q <= 8) {   // register-accumulating kernel, columns in chunks of 8 CPW
+        const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
+        constexpr int CPW = 4;
+        for (int a0 = 0; a0 < p; a0 += 8 * CPW) {
+            const int pc = std::min(p - a0, 8 * CPW);
+            const double2* Xc = X + (size_t)a0 * N;
+            double2* pp = partial + (size_t)a0 * q * nblk;
+            if (Q == 1) k_gemm_tn2<1, CPW><<<nblk, 256, 0, st>>>(Xc, pc, Y, q, N, pp);
+            else if (Q == 2) k_gemm_tn2<2, CPW><<<nblk, 256, 0, st>>>(Xc, pc, Y, q, N, pp);
+            else if (Q == 4) k_gemm_tn2<4, CPW><<<nblk, 256, 0, st>>>(Xc, pc, Y, q, N, pp);
+            else k_gemm_tn2<8, 2><<<nblk, 256, 0, st>>>(Xc, pc, Y, q, N, pp);
+            if (Q == 8 && pc > 16) {   // CPW = 2 covers 16 columns: second half of the chunk
+                k_gemm_tn2<8, 2><<<nblk, 256, 0, st>>>(Xc + (size_t)16 * N, pc - 16, Y, q, N, pp + (size_t)16 * q * nblk);
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
     if (q > 8) return cudaErrorInvalidValue;
     const int slice = 512;

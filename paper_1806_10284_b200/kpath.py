@@ -255,14 +255,35 @@ def default_store():
 _CALLS = [0]   # solve_path calls in this process (all ranks call it alike): store key prefix
 
 
-def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, stream=None, steal=True, **opts):
+class _Locked:
+    """Thread-safe iteration over a k index sequence (list or StealQueue)."""
+
+    def __init__(self, it):
+        import threading
+        self._it = iter(it)
+        self._lock = threading.Lock()
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        with self._lock:
+            return next(self._it)
+
+
+def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, stream=None, steal=True, per_gpu=1,
+               **opts):
     """Band structure along a k-path: every rank (torch.distributed, one
     process per GPU, if initialised) solves its LPT share on its own device
     through the C ABI, stealing unclaimed k from slower ranks when its own
     share is done (``steal``), and the merged, path-ordered records are
-    returned on every rank.  ``eps``: (3n,) float64 host array (P:L323-332
-    layout)."""
+    returned on every rank.  ``per_gpu`` > 1 runs that many solvers
+    concurrently on the rank's GPU (one host thread and one CUDA stream each;
+    the C ABI releases the GIL), which fills the device at small grids
+    (2-4 k-points per GPU at 64^3).  ``eps``: (3n,) float64
+    host array (P:L323-332 layout)."""
     import glob
+    import threading
 
     import torch.distributed as dist
 
@@ -273,19 +294,50 @@ def solve_path(a_raw, n, eps, kappas, nev, device=None, checkpoint_dir=None, str
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", "0"))
     lat = Lattice(a_raw, n)
-    S = Solver(lat, device=device, stream=stream, **opts)
-    S.set_epsilon(eps)
     shares = assign(kappas, world)
     store = default_store() if (steal and world > 1) else None
     _CALLS[0] += 1
     todo = StealQueue(shares, rank, store, prefix="kpath%d" % _CALLS[0]) if store is not None else shares[rank]
     ck = os.path.join(checkpoint_dir, "kpath_rank%d.jsonl" % rank) if checkpoint_dir else None
-    others = sorted(glob.glob(os.path.join(checkpoint_dir, "kpath_rank*.jsonl"))) if checkpoint_dir else []
+    others = sorted(glob.glob(os.path.join(checkpoint_dir, "kpath_rank*.jsonl*"))) if checkpoint_dir else []
     meta = run_meta(nev, eps, n=tuple(n), **{k: v for k, v in opts.items()})
+    if per_gpu <= 1:
+        S = Solver(lat, device=device, stream=stream, **opts)
+        S.set_epsilon(eps)
 
-    def solve(kap):
-        return S.solve(kap, nev, allow_noconv=True)
+        def solve(kap):
+            return S.solve(kap, nev, allow_noconv=True)
 
-    recs = run_path(solve, kappas, todo, rank=rank, checkpoint=ck, meta=meta, resume_from=others)
-    S.close()
-    return gather(recs, len(kappas))
+        recs = run_path(solve, kappas, todo, rank=rank, checkpoint=ck, meta=meta, resume_from=others)
+        S.close()
+        return gather(recs, len(kappas))
+    import torch
+    queue = _Locked(todo)
+    streams = [torch.cuda.Stream(device=device) for _ in range(per_gpu)]
+    solvers = []
+    for q in range(per_gpu):
+        S = Solver(lat, device=device, stream=streams[q].cuda_stream, **opts)
+        S.set_epsilon(eps)
+        solvers.append(S)
+    results = [[] for _ in range(per_gpu)]
+    errors = []
+
+    def worker(q):
+        try:
+            S = solvers[q]
+            results[q] = run_path(lambda kap: S.solve(kap, nev, allow_noconv=True), kappas, queue, rank=rank,
+                                  checkpoint=(ck + ".t%d" % q) if ck else None, meta=meta,
+                                  resume_from=others)
+        except Exception as e:  # noqa: BLE001 -- re-raised below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(q,)) for q in range(per_gpu)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for S in solvers:
+        S.close()
+    if errors:
+        raise errors[0]
+    return gather([r for rs in results for r in rs], len(kappas))

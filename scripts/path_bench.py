@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--out", default=None)
     ap.add_argument("--warm", type=int, default=1)
+    ap.add_argument("--per-gpu", type=int, default=1, help="concurrent solvers (streams) per GPU")
     a = ap.parse_args()
     gold = goldens()
     res = []
@@ -49,7 +50,7 @@ def main():
         ks = kappas(cfg, lat)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm)
+        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=a.per_gpu)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         dev = []

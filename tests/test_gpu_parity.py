@@ -686,3 +686,20 @@ def test_field_postprocessing_h_and_divergence(bnf):
         div = C1.conj().T @ D[:n] + C2.conj().T @ D[n:2 * n] + C3.conj().T @ D[2 * n:]
         scale = max(np.linalg.norm(C1.conj().T @ D[:n]), 1e-300)
         assert np.linalg.norm(div) <= 1e-10 * scale, (i, np.linalg.norm(div) / scale)
+
+
+def test_kpath_concurrent_solvers_per_gpu(bnf, tmp_path):
+    """kpath.solve_path with 2 concurrent solvers on one GPU (two host threads,
+    two CUDA streams; SURVEY §8(e) small-grid k-point concurrency) returns,
+    in path order, the eigenvalues of one solver to 1e-10."""
+    from paper_1806_10284_b200 import kpath
+    cfg = configs.config(2)
+    n = (16, 16, 16)
+    O = olat.snap(cfg.a_raw, n)
+    eps = E.stacked(E.sample(cfg.shape, n, O.a, O.delta, O.a_canon))
+    kaps = [tuple(olat.kvec_reduce(O, K)) for K in cfg.kpoints[:6]]
+    one = kpath.solve_path(cfg.a_raw, n, eps, kaps, 6, device=0)
+    two = kpath.solve_path(cfg.a_raw, n, eps, kaps, 6, device=0, per_gpu=2, checkpoint_dir=str(tmp_path))
+    assert [r.index for r in two] == list(range(6)) and all(r.status == "ok" for r in two)
+    for a, b in zip(one, two):
+        np.testing.assert_allclose(b.lam, a.lam, rtol=1e-10)
