@@ -160,7 +160,12 @@ struct PlaneTCfg {
     static constexpr size_t smem = off_bar + 64 + 1024;   // + alignment slack
 };
 
-template <int N1, int N2, int CG>
+// XS = 0: sequence w = tid % 16 with its N2 threads in different warps, the FFT
+// stage exchange in place in the strip buffer (block barriers); XS = 1: the N2
+// threads of a sequence are consecutive lanes of one warp and the exchange is
+// an xor-shuffle transpose (fastfft warp_xpose): shared memory then only
+// carries the strip staging, and the strip needs no barrier until its store.
+template <int N1, int N2, int CG, int XS>
 __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <= 128 ? 2 : 1)
     k_plane_t(OpArgs a, CGFuse cgf, const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap mx,
               int zbase) {
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
     unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + C::off_bar);
     const ModeP& p = a.mp;
     const int tid = threadIdx.x;
-    const int w = tid % S, t = tid / S;
+    const int w = XS ? (tid / 32) * (32 / N2) + (tid % 32) / N2 : tid % S;
+    const int t = XS ? tid % N2 : tid / S;
     const int c = blockIdx.x;
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
@@ -226,6 +232,7 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
         bulk_commit();
     };
     if (tid == 0) load(0);
+    static_assert(!XS || 32 % N2 == 0, "warp-local exchange: N2 divides 32");
     const unsigned n12 = (unsigned)p.n12;
     const unsigned long long s3 = (unsigned long long)p.n3;
     double pmp = 0.0;
@@ -245,7 +252,12 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
             const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
             for (int m = 0; m < N1; ++m) v[m] = b[LayY<N>::at(w, N2 * m + t)];
-            fft_fwd_ip<N1, N2, 1, LayY<N>>(v, t, w, b, ry);
+            if constexpr (XS) {
+                fast::fft_fwd_w<N1, N2, 1, 1>(v, t, w, nullptr, ry);
+                __syncwarp();   // the sequence's lanes have read their inputs before the outputs overwrite them
+            } else {
+                fft_fwd_ip<N1, N2, 1, LayY<N>>(v, t, w, b, ry);
+            }
             const double2 wt = conj2t(tw_at_t(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
             const double2 wu = conj2t(tw_at_t(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
             const double2 wk = conj2t(tw_at_t(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3));
@@ -260,7 +272,8 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
             const int brow = r * S + w;
 #pragma unroll
             for (int m = 0; m < N1; ++m) v[m] = b[LayX::at(w, N2 * m + t)];
-            fft_fwd_ip<N1, N2, 1, LayX>(v, t, w, b, rx);
+            if constexpr (XS) fast::fft_fwd_w<N1, N2, 1, 1>(v, t, w, nullptr, rx);
+            else fft_fwd_ip<N1, N2, 1, LayX>(v, t, w, b, rx);
             const size_t rowofs = (size_t)l * p.n + (size_t)N * ((size_t)brow + (size_t)N * c);
             auto scale = [&](auto eps_at) {
 #pragma unroll
@@ -277,7 +290,8 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
             if (epf) scale([&](int aa) { return lut_s[eps_s[brow * N + aa]]; });
             else if (a.eps_idx) scale([&](int aa) { return lut_s[__ldg(a.eps_idx + rowofs + aa)]; });
             else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
-            fft_mirror_ip<N1, N2, -1, LayX>(v, t, w, b, rx);
+            if constexpr (XS) fast::fft_mirror_w<N1, N2, -1, 1>(v, t, w, nullptr, rx);
+            else fft_mirror_ip<N1, N2, -1, LayX>(v, t, w, b, rx);
 #pragma unroll
             for (int m = 0; m < N1; ++m) b[LayX::at(w, N2 * m + t)] = v[m];
         } else {   // ---------------- conj twiddle, y-DFT (-) ----------------
@@ -288,7 +302,12 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
             const double2 wt = tw_at_t(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
             const double2 wu = tw_at_t(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
             fast::twiddle_natural<N1, N2>(v, wt, wu);
-            fft_fwd_ip<N1, N2, -1, LayY<N>>(v, t, w, b, ry);
+            if constexpr (XS) {
+                fast::fft_fwd_w<N1, N2, -1, 1>(v, t, w, nullptr, ry);
+                __syncwarp();
+            } else {
+                fft_fwd_ip<N1, N2, -1, LayY<N>>(v, t, w, b, ry);
+            }
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -327,8 +346,12 @@ cudaError_t launch_plane_t_t(const OpArgs& a, int nslab, const CGFuse* cg, cudaS
         kern<<<g, C::NT, C::smem, st>>>(a, cgarg, my, mx, zbase);
         return cudaGetLastError();
     };
-    if (cg) return run(k_plane_t<N1, N2, 1>, *cg);
-    return run(k_plane_t<N1, N2, 0>, CGFuse{});
+    if (a.plane_t == 2) {
+        if (cg) return run(k_plane_t<N1, N2, 1, 1>, *cg);
+        return run(k_plane_t<N1, N2, 0, 1>, CGFuse{});
+    }
+    if (cg) return run(k_plane_t<N1, N2, 1, 0>, *cg);
+    return run(k_plane_t<N1, N2, 0, 0>, CGFuse{});
 }
 
 }  // namespace

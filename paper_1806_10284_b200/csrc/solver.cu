@@ -551,7 +551,7 @@ cudaError_t slab_exchange(bnf_solver* s, double2* U, double2* Ub, int nvec, int 
 }
 
 const char* plane_name(const OpArgs& a, bool cg) {
-    if (a.plane_t) return cg ? "plane_t_cg" : "plane_t";
+    if (a.plane_t) return a.plane_t == 2 ? (cg ? "plane_ts_cg" : "plane_ts") : (cg ? "plane_t_cg" : "plane_t");
     if (a.plane_w) return a.plane_w == 2 ? (cg ? "plane_ws_cg" : "plane_ws") : (cg ? "plane_w_cg" : "plane_w");
     if (a.plane_l2) return cg ? "plane_l2_cg" : "plane_l2";
     return cg ? "plane_cg" : "plane";
@@ -650,7 +650,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
         std::getenv("BNF_PLANE_T")) {
         s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? std::atoi(std::getenv("BNF_PLANE_L2")) : 0;
         s->args.plane_w = std::getenv("BNF_PLANE_W") ? std::atoi(std::getenv("BNF_PLANE_W")) : 0;
-        s->args.plane_t = (std::getenv("BNF_PLANE_T") && s->plane_t_ok) ? 1 : 0;
+        s->args.plane_t = (std::getenv("BNF_PLANE_T") && s->plane_t_ok) ? std::max(1, std::atoi(std::getenv("BNF_PLANE_T"))) : 0;
         if (std::getenv("BNF_NO_PLANE")) s->args.plane_w = s->args.plane_t = 0;
         s->use_plane = std::getenv("BNF_NO_PLANE") == nullptr;
         s->kver++;
@@ -667,10 +667,10 @@ int autotune_plane(bnf_solver* s, int nvec) {
     CK(cudaEventCreate(&e1));
     // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2,
     // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles),
-    // 5 = plane via L2 staged by TMA
-    const int nvar = s->plane_t_ok ? 6 : plane_w_supported(s->args) ? 5 : 3;
+    // 5 / 6 = plane via L2 staged by TMA (exchange in shared memory / by warp shuffles)
+    const int nvar = s->plane_t_ok ? 7 : plane_w_supported(s->args) ? 5 : 3;
     const int v0 = s->nsl > 1 ? 2 : 0;   // slab mode: plane passes through L2 only (slab-aware)
-    float best[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float best[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;
@@ -678,10 +678,10 @@ int autotune_plane(bnf_solver* s, int nvec) {
         s->use_plane = variant >= 1;
         s->args.plane_l2 = variant == 2 ? 1 : 0;
         s->args.plane_w = (variant == 3 || variant == 4) ? variant - 2 : 0;
-        s->args.plane_t = variant == 5 ? 1 : 0;
+        s->args.plane_t = variant >= 5 ? variant - 4 : 0;
     };
     for (int variant = v0; variant < nvar; ++variant) {
-        if (s->nsl > 1 && variant == 5) continue;   // TMA plane: one slab only
+        if (s->nsl > 1 && variant >= 5) continue;   // TMA plane: one slab only
         set(variant);
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
         CK(cudaEventRecord(e0, s->st));
