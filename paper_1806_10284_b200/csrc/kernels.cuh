@@ -67,7 +67,8 @@ struct OpArgs {
     long long nloc;
     long long vsf;              // Fourier-side vector stride (elements): 2 nloc, or 2n for virtual slabs
     long long nblk;             // n1 n2loc n3loc: one (slab pair, vector, component) exchange block
-    int zcfg;                   // z-pass variant: bit 0 = stage x / r tiles with the inputs (CG), bit 1 = half-width tiles
+    int zcfg;                   // z-pass variant: bit 0 = stage x / r tiles with the inputs (CG), bit 1 = half-width
+                                // tiles, bit 2 = CG residual of zadj prefetched into registers before the mode loop
     int plane_t;                // plane pass staged by TMA (plane_tma.cu)
 };
 

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             cp_async16(sm + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 0, c, kstride));
             cp_async16(sm + TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 1, c, kstride));
             cp_async16(sm + 2 * TE + q, u0 + g + u_row<SL>(a, gridDim.z, vec, 2, c, kstride));
-            if (MODE == 1 && RST) {   // residual tile staged with U: every load of the tile in flight at once
+            if (MODE == 1 && RST == 1) {   // residual tile staged with U: every load of the tile in flight at once
                 const double2* r0 = OUT + (size_t)vec * a.vsf + col0 + g + kstride * (size_t)c;
                 cp_async16(sm + 3 * TE + q, r0);
                 cp_async16(sm + 4 * TE + q, r0 + n);
@@ -250,8 +250,10 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
     double2* o1 = OUT + (size_t)vec * a.vsf + gcol;
+    constexpr int J = (TE + NT - 1) / NT;   // elements per thread in the mode loop
+    double2 rb1[RST == 2 ? J : 1], rb2[RST == 2 ? J : 1];
     double2 rn1 = make_double2(0, 0), rn2 = make_double2(0, 0);
-    if (MODE == 1 && !RST && tid < TE) {   // first residual element, in flight during the FFT phase
+    if (MODE == 1 && RST == 0 && tid < TE) {   // first residual element, in flight during the FFT phase
         rn1 = o1[kstride * (tid / W)];
         rn2 = o1[n + kstride * (tid / W)];
     }
@@ -273,10 +275,20 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) ct[(t + N2 * u + N1 * k2) * W + w] = v[u * N2 + k2];
     }
+    if (MODE == 1 && RST == 2) {   // every residual element of this thread in flight across the barrier
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+            const int e = tid + jj * NT;
+            if (e < TE) {
+                rb1[jj] = o1[kstride * (e / W)];
+                rb2[jj] = o1[n + kstride * (e / W)];
+            }
+        }
+    }
     __syncthreads();
     // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
     double rr = 0.0;
-#pragma unroll 1
+#pragma unroll(RST == 2 ? J : 1)
     for (int e = tid; e < TE; e += NT) {
         const int k = e / W;
         const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
@@ -289,8 +301,9 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         z1 = cscale(z1, o.f1);
         z2 = cscale(z2, o.f2);
         if (MODE == 1) {
-            double2 r1 = RST ? sm[3 * TE + e] : rn1, r2 = RST ? sm[4 * TE + e] : rn2;
-            if (!RST && e + NT < TE) {
+            double2 r1 = RST == 1 ? sm[3 * TE + e] : (RST == 2 ? rb1[(e - tid) / NT] : rn1);
+            double2 r2 = RST == 1 ? sm[4 * TE + e] : (RST == 2 ? rb2[(e - tid) / NT] : rn2);
+            if (RST == 0 && e + NT < TE) {
                 rn1 = o1[kstride * ((e + NT) / W)];
                 rn2 = o1[n + kstride * ((e + NT) / W)];
             }
@@ -333,7 +346,7 @@ template <int N1, int N2, int W>
 struct ZLaunch {
     using C = ZCfg<N1, N2, W>;
     static size_t smem_fwd(int mode, int rst) { return (size_t)(mode ? (rst ? 6 : 4) : 3) * C::TE * sizeof(double2); }
-    static size_t smem_adj(int mode, int rst) { return (size_t)(mode && rst ? 5 : 3) * C::TE * sizeof(double2); }
+    static size_t smem_adj(int mode, int rst) { return (size_t)(mode && rst == 1 ? 5 : 3) * C::TE * sizeof(double2); }
 };
 
 }  // namespace
@@ -376,7 +389,7 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
                            cudaStream_t st) {
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
-    const int rst = (a.zcfg & 1) && mode;
+    const int rst = !mode ? 0 : (a.zcfg & 4) ? 2 : (a.zcfg & 1) ? 1 : 0;
     const size_t smem = L::smem_adj(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, CGFuse cgv) -> cudaError_t {
@@ -386,6 +399,7 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if (mode && rst == 2) return sl ? go(k_zadj2<N1, N2, W, 1, 1, 2>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0, 2>, 1, *cg);
     if (mode && rst) return sl ? go(k_zadj2<N1, N2, W, 1, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0, 1>, 1, *cg);
     if (mode) return sl ? go(k_zadj2<N1, N2, W, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0>, 1, *cg);
     return sl ? go(k_zadj2<N1, N2, W, 0, 1>, op, CGFuse{}) : go(k_zadj2<N1, N2, W, 0, 0>, op, CGFuse{});
