@@ -1288,7 +1288,8 @@ static cudaError_t set_smem(const void* f, size_t bytes) {
 }
 
 cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st) {
-    if (a.fast && has_fast(a.mp.n3)) return fast_zfwd(a, Y, U, nvec, op, st);
+    // op 2 (H field, bnf_eigvecs BNF_VEC_H) exists only in the generic pass
+    if (op != 2 && a.fast && has_fast(a.mp.n3)) return fast_zfwd(a, Y, U, nvec, op, st);
     const size_t sm = smem_z(a);
     cudaError_t e = set_smem((const void*)k_zfwd, sm);
     if (e != cudaSuccess) return e;
