@@ -144,14 +144,14 @@ __device__ __forceinline__ void fft_mirror_ip(double2 (&v)[N1], int t, int w, do
     fast::DFT<N1, S>::run(v);
 }
 
-template <int N1, int N2>
+template <int N1, int N2, int XS = 0>
 struct PlaneTCfg {
     static constexpr int N = N1 * N2;
     static constexpr int S = 16;                 // sequences per strip
     static constexpr int P = N / S;              // strips per phase
     static constexpr int NT = S * N2;            // threads
     static constexpr int SE = S * N;             // complex elements per strip buffer
-    static constexpr bool EPF = N <= 128;        // whole-plane eps index prefetch
+    static constexpr bool EPF = N <= 128 && !XS;  // whole-plane eps index prefetch (XS: 3 CTAs / SM instead)
     // dynamic smem: 2 strip buffers (1024-aligned), roots, lut, eps, barriers
     static constexpr size_t off_root = (size_t)2 * SE * 16;
     static constexpr size_t off_lut = off_root + (size_t)2 * N * 16;
@@ -166,10 +166,10 @@ struct PlaneTCfg {
 // an xor-shuffle transpose (fastfft warp_xpose): shared memory then only
 // carries the strip staging, and the strip needs no barrier until its store.
 template <int N1, int N2, int CG, int XS>
-__global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <= 128 ? 2 : 1)
+__global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, XS>::NT <= 128 ? (XS ? 3 : 2) : 1)
     k_plane_t(OpArgs a, CGFuse cgf, const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap mx,
               int zbase) {
-    using C = PlaneTCfg<N1, N2>;
+    using C = PlaneTCfg<N1, N2, XS>;
     constexpr int N = C::N, S = C::S, P = C::P, NT = C::NT, SE = C::SE;
     extern __shared__ unsigned char smraw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(smraw) + 1023) & ~(size_t)1023);
@@ -338,20 +338,21 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2>::NT, PlaneTCfg<N1, N2>::NT <
 template <int N1, int N2>
 cudaError_t launch_plane_t_t(const OpArgs& a, int nslab, const CGFuse* cg, cudaStream_t st, const CUtensorMap& my,
                              const CUtensorMap& mx, int zbase) {
-    using C = PlaneTCfg<N1, N2>;
     const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
-    auto run = [&](auto kern, auto cgarg) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    auto run = [&](auto kern, auto cgarg, size_t smem, int nt) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<g, C::NT, C::smem, st>>>(a, cgarg, my, mx, zbase);
+        kern<<<g, nt, smem, st>>>(a, cgarg, my, mx, zbase);
         return cudaGetLastError();
     };
+    using C0 = PlaneTCfg<N1, N2, 0>;
+    using C1 = PlaneTCfg<N1, N2, 1>;
     if (a.plane_t == 2) {
-        if (cg) return run(k_plane_t<N1, N2, 1, 1>, *cg);
-        return run(k_plane_t<N1, N2, 0, 1>, CGFuse{});
+        if (cg) return run(k_plane_t<N1, N2, 1, 1>, *cg, C1::smem, C1::NT);
+        return run(k_plane_t<N1, N2, 0, 1>, CGFuse{}, C1::smem, C1::NT);
     }
-    if (cg) return run(k_plane_t<N1, N2, 1, 0>, *cg);
-    return run(k_plane_t<N1, N2, 0, 0>, CGFuse{});
+    if (cg) return run(k_plane_t<N1, N2, 1, 0>, *cg, C0::smem, C0::NT);
+    return run(k_plane_t<N1, N2, 0, 0>, CGFuse{}, C0::smem, C0::NT);
 }
 
 }  // namespace
