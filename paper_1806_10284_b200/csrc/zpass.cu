@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             if (MODE == 1) {
                 cp_async16(sm + 2 * TE + q, p1 + g);
                 cp_async16(sm + 3 * TE + q, p1 + n + g);
-                if (RST) {   // x staged too: every input of the tile in flight at once
+                if (RST == 1) {   // x staged too: every input of the tile in flight at once
                     const double2* x1 = Xcg + (size_t)vec * a.vsf + col0;
                     cp_async16(sm + 4 * TE + q, x1 + g);
                     cp_async16(sm + 5 * TE + q, x1 + n + g);
@@ -137,27 +137,40 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     }
     const double alpha_prev = MODE ? cg.alpha[vec] : 0.0;
     const double beta = MODE ? cg.beta[vec] : 0.0;
+    const int w = tid % W;
+    const size_t gcol = col0 + w;
+    double2* xcol = MODE ? Xcg + (size_t)vec * a.vsf + gcol : nullptr;
+    constexpr int J = (TE + NT - 1) / NT;   // elements per thread in the mode loop
+    double2 xb1[RST == 2 ? J : 1], xb2[RST == 2 ? J : 1];
+    if (MODE == 1 && RST == 2) {   // every x element of this thread in flight with the r / p tile
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+            const int e = tid + jj * NT;
+            if (e < TE) {
+                xb1[jj] = xcol[kstride * (e / W)];
+                xb2[jj] = xcol[n + kstride * (e / W)];
+            }
+        }
+    }
     cp_async_wait0();
     __syncthreads();
-    const int w = tid % W;
     const ColS& c = cs[w];
-    const size_t gcol = col0 + w;
     // x is streamed straight from HBM (not staged), one element ahead
-    double2* xcol = MODE ? Xcg + (size_t)vec * a.vsf + gcol : nullptr;
     double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0);
-    if (MODE == 1 && !RST && tid < TE) {
+    if (MODE == 1 && RST == 0 && tid < TE) {
         xn1 = xcol[kstride * (tid / W)];
         xn2 = xcol[n + kstride * (tid / W)];
     }
     // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
-#pragma unroll 1
+#pragma unroll(RST == 2 ? J : 1)
     for (int e = tid; e < TE; e += NT) {
         const int k = e / W;
         double2 u1 = sm[e], u2 = sm[TE + e];
         if (MODE == 1) {
             const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
-            const double2 x1 = RST ? sm[4 * TE + e] : xn1, x2 = RST ? sm[5 * TE + e] : xn2;
-            if (!RST && e + NT < TE) {
+            const double2 x1 = RST == 1 ? sm[4 * TE + e] : (RST == 2 ? xb1[(e - tid) / NT] : xn1);
+            const double2 x2 = RST == 1 ? sm[5 * TE + e] : (RST == 2 ? xb2[(e - tid) / NT] : xn2);
+            if (RST == 0 && e + NT < TE) {
                 xn1 = xcol[kstride * ((e + NT) / W)];
                 xn2 = xcol[n + kstride * ((e + NT) / W)];
             }
@@ -345,7 +358,7 @@ __global__ void k_cg_xfinal(double2* __restrict__ X, const double2* __restrict__
 template <int N1, int N2, int W>
 struct ZLaunch {
     using C = ZCfg<N1, N2, W>;
-    static size_t smem_fwd(int mode, int rst) { return (size_t)(mode ? (rst ? 6 : 4) : 3) * C::TE * sizeof(double2); }
+    static size_t smem_fwd(int mode, int rst) { return (size_t)(mode ? (rst == 1 ? 6 : 4) : 3) * C::TE * sizeof(double2); }
     static size_t smem_adj(int mode, int rst) { return (size_t)(mode && rst == 1 ? 5 : 3) * C::TE * sizeof(double2); }
 };
 
@@ -368,7 +381,7 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
                            const CGFuse* cg, cudaStream_t st) {
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
-    const int rst = (a.zcfg & 1) && mode;
+    const int rst = !mode ? 0 : (a.zcfg & 4) ? 2 : (a.zcfg & 1) ? 1 : 0;
     const size_t smem = L::smem_fwd(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, double2* Pp, double2* Xp, CGFuse cgv) -> cudaError_t {
@@ -378,6 +391,7 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if (mode && rst == 2) return sl ? go(k_zfwd2<N1, N2, W, 1, 1, 2>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0, 2>, 1, P, X, *cg);
     if (mode && rst) return sl ? go(k_zfwd2<N1, N2, W, 1, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0, 1>, 1, P, X, *cg);
     if (mode) return sl ? go(k_zfwd2<N1, N2, W, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0>, 1, P, X, *cg);
     return sl ? go(k_zfwd2<N1, N2, W, 0, 1>, op, nullptr, nullptr, CGFuse{})
