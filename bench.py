@@ -243,6 +243,7 @@ def main():
     ap.add_argument("--guard", type=int, default=2)
     ap.add_argument("--warm", type=int, default=1,
                     help="start each k-point from the previous one's Ritz vectors (DESIGN R17)")
+    ap.add_argument("--kstart", type=int, default=12, help="path index of the first timed k-point")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -285,8 +286,12 @@ def main():
 
     share = kpath.assign(ks, world)[rank]   # LPT share of the path (no data-path collective)
 
+    # the timed steps start at path point --kstart (k12 by default: the middle of the path, whose oracle
+    # golden exists; with --steps 12 or more the timed k-points also cover k23 and k0 = Gamma)
+    off = (share.index(args.kstart) - args.warmup) % len(share) if args.kstart in share else 0
+
     def kidx(step):
-        return share[step % len(share)]
+        return share[(step + off) % len(share)]
 
     def barrier():
         if world > 1:

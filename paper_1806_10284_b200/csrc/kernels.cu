@@ -1371,8 +1371,10 @@ cudaError_t launch_dot_final(const double2* partial, int nblk, int nvec, double2
 
 cudaError_t launch_gemm_tn_partial(const double2* X, int p, const double2* Y, int q, long long N, double2* partial,
                                    int nblk, cudaStream_t st) {
-    static const bool v1 = std::getenv("BNF_GEMM_V1") != nullptr;
-    if (!v1 && q <= 8) {   // register-accumulating kernel, columns in chunks of 8 CPW
+    // register-accumulating kernel: opt-in (BNF_GEMM_V2) -- measured 1.8x slower than the per-slice
+    // kernel below at the bench workload (fewer loads in flight per warp), kept for the record
+    static const bool v2 = std::getenv("BNF_GEMM_V2") != nullptr;
+    if (v2 && q <= 8) {   // columns in chunks of 8 CPW
         const int Q = q <= 1 ? 1 : (q <= 2 ? 2 : (q <= 4 ? 4 : 8));
         constexpr int CPW = 4;
         for (int a0 = 0; a0 < p; a0 += 8 * CPW) {

@@ -69,6 +69,7 @@ struct OpArgs {
     long long nblk;             // n1 n2loc n3loc: one (slab pair, vector, component) exchange block
     int zcfg;                   // z-pass variant: bit 0 = stage x / r tiles with the inputs (CG), bit 1 = half-width
                                 // tiles, bit 2 = CG residual of zadj prefetched into registers before the mode loop
+                                // (default on), bit 3 = CG x of zfwd prefetched into registers (measured slower)
     int plane_t;                // plane pass staged by TMA (plane_tma.cu)
 };
 

@@ -1357,7 +1357,9 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.nloc = n;
     s->args.vsf = 2 * n;
     s->args.nblk = n;
-    s->args.zcfg = std::getenv("BNF_ZCFG") ? std::atoi(std::getenv("BNF_ZCFG")) : 0;
+    // z-pass variant (kernels.cuh): default = register prefetch of the CG residual in zadj2
+    // (128^3, b = 2: 143 vs 149 us; the other bits measured no faster, profiles/r02_*)
+    s->args.zcfg = std::getenv("BNF_ZCFG") ? std::atoi(std::getenv("BNF_ZCFG")) : 4;
     s->args.fast = (std::getenv("BNF_NO_FAST") == nullptr) ? 1 : 0;
     // tile widths: keep each kernel's shared memory <= ~100 KB
     const int budget = 100 * 1024;

@@ -381,7 +381,7 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
                            const CGFuse* cg, cudaStream_t st) {
     using L = ZLaunch<N1, N2, W>;
     const int mode = cg ? 1 : 0;
-    const int rst = !mode ? 0 : (a.zcfg & 4) ? 2 : (a.zcfg & 1) ? 1 : 0;
+    const int rst = !mode ? 0 : (a.zcfg & 8) ? 2 : (a.zcfg & 1) ? 1 : 0;   // x prefetch measured slower: off
     const size_t smem = L::smem_fwd(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, double2* Pp, double2* Xp, CGFuse cgv) -> cudaError_t {
