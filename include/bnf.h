@@ -160,6 +160,11 @@ typedef struct {
                                    j = r n2/P + jl), real-space work in z-slabs of n3/P planes.
                                    Needs n2, n3 divisible by P, a square xy plane of 64/128/256.
                                    bnf_apply_Ar / BNF_VEC_Y use that layout; BNF_VEC_E is refused. */
+    int relax_inner;            /* 0 (default, the paper's fixed tol_inner).  1: NEXT-1 inexact
+                                   inner solves -- Lanczos step j solves to tol_inner * clamp(1e-6 /
+                                   res_{j-1}, 1, 1e5), res = the largest relative Ritz residual of the
+                                   wanted pairs; the final Rayleigh-Ritz + residual polish (res_tol,
+                                   exact inner tolerance) secure the returned pairs. */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);

@@ -391,6 +391,7 @@ struct bnf_solver {
     double2* h_small = nullptr;  // pinned scratch for small matrices
     size_t h_small_cap = 0;
     int nblk = 592;
+    double tol_inner_eff = 0.0;   // relaxed inner tolerance of the current Lanczos step (opts.relax_inner), 0 = tol_inner
     int nsl = 1;              // slabs of the decomposition (opts.slabs, or the ranks of bnf_solver_create_dist)
     bool dist = false;        // one slab per process (NCCL), this process = slab `rank`
     int rank = 0;
@@ -739,7 +740,7 @@ int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_o
     RUN("copy", launch_copy(R, C, N * nvec, s->st));
     RUN("copy", launch_copy(P, C, N * nvec, s->st));
     TRY(dots(s, R, R, N, nvec, dd));
-    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->o.tol_inner, s->st));
+    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->tol_inner_eff > 0.0 ? s->tol_inner_eff : s->o.tol_inner, s->st));
     int it = 0;
     for (; it < s->o.max_inner; ++it) {
         TRY(apply_op(s, P, MP, nvec, BNF_OP_M));
@@ -904,7 +905,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     CK(cudaMemsetAsync(P, 0, vb, s->st));
     RUN("copy", launch_copy(R, C, N * nvec, s->st));
     TRY(dots(s, R, R, N, nvec, dd));
-    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->o.tol_inner, s->st));
+    RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->tol_inner_eff > 0.0 ? s->tol_inner_eff : s->o.tol_inner, s->st));
     CK(cudaMemsetAsync(s->cgs.beta, 0, nvec * sizeof(double), s->st));
     CK(cudaMemsetAsync(s->cgf.alpha, 0, nvec * sizeof(double), s->st));
     CGFuse cg = s->cgf;
@@ -1256,6 +1257,7 @@ void bnf_opts_default(bnf_opts* o) {
     o->res_tol = 5e-9;
     o->max_polish = 3;
     o->slabs = 1;
+    o->relax_inner = 0;
 }
 
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
@@ -1731,7 +1733,16 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         double2* Vj = V + (size_t)step * b * N;
         TRY(s->V.ensure(vbytes * (size_t)b * (step + 2)));
         double2* W = V + (size_t)(step + 1) * b * N;   // next block, built in place
+        // NEXT-1 relaxed inner solves (opts.relax_inner): the j-th application of A_r^{-1} may be
+        // less accurate once the wanted Ritz pairs have converged partly (inexact Krylov, the allowed
+        // error grows like 1 / residual): tol_j = tol_inner * clamp(1e-6 / res_{j-1}, 1, 1e5).  The
+        // final Rayleigh-Ritz on A_r and the R19 residual polish (exact inner tolerance) secure the
+        // returned pairs.
+        s->tol_inner_eff = 0.0;
+        if (s->o.relax_inner && step > 0 && maxres > 0.0)
+            s->tol_inner_eff = s->o.tol_inner * std::min(1e5, std::max(1.0, 1e-6 / maxres));
         TRY(apply_Ar_inv(s, Vj, W, b));  // W = A_r^{-1} V_j
+        s->tol_inner_eff = 0.0;
         // full reorthogonalisation (classical Gram-Schmidt against all of V) with the
         // DGKS / Kahan-Parlett "twice is enough" test: the second pass runs unless the
         // first kept every column's norm above 1/sqrt(2) of its value (norm after the
