@@ -625,11 +625,25 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double2* __restrict__ X,
             const int a = acol + 8 * j;
             if (a >= p || (p < 8 && j > 0)) break;
             const double2* xa = X + (size_t)a * N + s0;
-#pragma unroll 4
-            for (int r = r0 + lane; r < r1; r += 32) {
-                const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
+            asm volatile("" ::: "memory");   // one column's loads at a time (register budget)
+            if (parts == 1) {   // whole slice: all SL / 32 loads of the column in flight
+                double2 x[SL / 32];
 #pragma unroll
-                for (int c = 0; c < Q; ++c) sum[j][c] = cadd(sum[j][c], cjmul(x, ys[c * SL + r]));
+                for (int k = 0; k < SL / 32; ++k) {
+                    const int r = lane + 32 * k;
+                    x[k] = (s0 + r < N) ? xa[r] : make_double2(0, 0);
+                }
+#pragma unroll
+                for (int k = 0; k < SL / 32; ++k)
+#pragma unroll
+                    for (int c = 0; c < Q; ++c) sum[j][c] = cadd(sum[j][c], cjmul(x[k], ys[c * SL + lane + 32 * k]));
+            } else {
+#pragma unroll 4
+                for (int r = r0 + lane; r < r1; r += 32) {
+                    const double2 x = (s0 + r < N) ? xa[r] : make_double2(0, 0);
+#pragma unroll
+                    for (int c = 0; c < Q; ++c) sum[j][c] = cadd(sum[j][c], cjmul(x, ys[c * SL + r]));
+                }
             }
         }
     }
