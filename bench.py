@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--warm", type=int, default=1,
                     help="start each k-point from the previous one's Ritz vectors (DESIGN R17)")
     ap.add_argument("--kstart", type=int, default=12, help="path index of the first timed k-point")
+    ap.add_argument("--relax-inner", type=int, default=0,
+                    help="NEXT-1 inexact inner CG (bnf_opts.relax_inner); default 0 = the paper's fixed 1e-13")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -280,7 +282,7 @@ def main():
     ks = kappas(cfg, lat)
     stream = torch.cuda.Stream()
     S = bnf.Solver(lat, device=local, stream=stream.cuda_stream, profile=0, block=args.block, guard=args.guard,
-                   warm=args.warm)
+                   warm=args.warm, relax_inner=args.relax_inner)
     S.set_epsilon(eps)
     nev = cfg.nev
 
@@ -433,7 +435,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "grid": list(cfg.n), "nev": nev, "kpoints_on_path": len(ks),
                    "block": args.block, "guard": args.guard, "tol_outer": 1e-12, "tol_inner": 1e-13,
-                   "warm_start": bool(args.warm),
+                   "warm_start": bool(args.warm), "relax_inner": bool(args.relax_inner),
                    "l2": "inputs larger than L2 (Krylov basis and work arrays >> 126 MB)",
                    "parallelism": "k-point replicas x%d" % world},
         "kpoints_per_s": kps,

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--warm", type=int, default=1)
     ap.add_argument("--per-gpu", type=int, default=1, help="concurrent solvers (streams) per GPU")
+    ap.add_argument("--relax-inner", type=int, default=0)
     a = ap.parse_args()
     gold = goldens()
     res = []
@@ -50,7 +51,8 @@ def main():
         ks = kappas(cfg, lat)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=a.per_gpu)
+        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=a.per_gpu,
+                                relax_inner=a.relax_inner)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         dev = []
