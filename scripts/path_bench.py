@@ -62,6 +62,7 @@ def main():
                 g = np.asarray(gold[key][:len(r.lam)])
                 dev.append(float(np.max(np.abs(np.asarray(r.lam[:len(g)]) - g) / g)))
         line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
+                "per_gpu": a.per_gpu, "relax_inner": a.relax_inner,
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "matvecs_per_kpoint": float(np.mean([r.stats["matvecs"] for r in recs])),
                 "max_residual": max(r.stats["max_residual"] for r in recs),
