@@ -152,15 +152,22 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             }
         }
     }
+    // x is streamed straight from HBM (not staged), two elements ahead; the first two are issued
+    // before the wait for the r / p tile so that their latency overlaps it
+    double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0), xm1 = xn1, xm2 = xn1;
+    if (MODE == 1 && RST == 0) {
+        if (tid < TE) {
+            xn1 = xcol[kstride * (tid / W)];
+            xn2 = xcol[n + kstride * (tid / W)];
+        }
+        if (tid + NT < TE) {
+            xm1 = xcol[kstride * ((tid + NT) / W)];
+            xm2 = xcol[n + kstride * ((tid + NT) / W)];
+        }
+    }
     cp_async_wait0();
     __syncthreads();
     const ColS& c = cs[w];
-    // x is streamed straight from HBM (not staged), one element ahead
-    double2 xn1 = make_double2(0, 0), xn2 = make_double2(0, 0);
-    if (MODE == 1 && RST == 0 && tid < TE) {
-        xn1 = xcol[kstride * (tid / W)];
-        xn2 = xcol[n + kstride * (tid / W)];
-    }
     // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
 #pragma unroll(RST == 2 ? J : 1)
     for (int e = tid; e < TE; e += NT) {
@@ -170,9 +177,13 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
             const double2 x1 = RST == 1 ? sm[4 * TE + e] : (RST == 2 ? xb1[(e - tid) / NT] : xn1);
             const double2 x2 = RST == 1 ? sm[5 * TE + e] : (RST == 2 ? xb2[(e - tid) / NT] : xn2);
-            if (RST == 0 && e + NT < TE) {
-                xn1 = xcol[kstride * ((e + NT) / W)];
-                xn2 = xcol[n + kstride * ((e + NT) / W)];
+            if (RST == 0) {
+                xn1 = xm1;
+                xn2 = xm2;
+                if (e + 2 * NT < TE) {
+                    xm1 = xcol[kstride * ((e + 2 * NT) / W)];
+                    xm2 = xcol[n + kstride * ((e + 2 * NT) / W)];
+                }
             }
             double2* xg = xcol + kstride * k;
             xg[0] = make_double2(fma(alpha_prev, q1.x, x1.x), fma(alpha_prev, q1.y, x1.y));   // x += alpha_prev p
