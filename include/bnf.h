@@ -165,6 +165,11 @@ typedef struct {
                                    res_{j-1}, 1, 1e5), res = the largest relative Ritz residual of the
                                    wanted pairs; the final Rayleigh-Ritz + residual polish (res_tol,
                                    exact inner tolerance) secure the returned pairs. */
+    int method;                 /* eigensolver: 0 (default) = the paper's inverse Lanczos with CG inner
+                                   solves; 1 = NEXT-1 LOBPCG on A_r preconditioned by
+                                   Sigma_r^{-2} (no inner solves; block nev + guard, soft locking),
+                                   stopping at ||A_r y - lambda y|| <= res_tol; max_outer = iteration
+                                   cap (0: 1000); block / tol_outer / tol_inner are not used. */
 } bnf_opts;
 
 void bnf_opts_default(bnf_opts* opts);

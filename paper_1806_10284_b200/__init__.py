@@ -45,7 +45,7 @@ class Opts(C.Structure):
                 ("block", C.c_int), ("guard", C.c_int), ("seed", C.c_ulonglong), ("refine", C.c_int),
                 ("profile", C.c_int), ("warm", C.c_int), ("reorth_once_ok", C.c_int),
                 ("res_tol", C.c_double), ("max_polish", C.c_int), ("slabs", C.c_int),
-                ("relax_inner", C.c_int)]
+                ("relax_inner", C.c_int), ("method", C.c_int)]
 
 
 class Stats(C.Structure):

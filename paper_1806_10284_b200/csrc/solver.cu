@@ -382,6 +382,7 @@ struct bnf_solver {
     long long graph_calls = 0;
     DevBuf hroot;             // e^{i pi k / n3}
     GrowBuf V;             // Lanczos basis (grows with the iteration, VMM-backed)
+    DevBuf lob;            // LOBPCG blocks X, AX, W, AW, P, AP and four scratch blocks (opts.method = 1)
     DevBuf Wb, AZ, Yv;     // work block, A_r * Ritz, Ritz vectors
     std::vector<double> lam;
     int nev_last = 0;
@@ -1122,6 +1123,255 @@ int set_kappa_impl(bnf_solver* s, const double kappa[3]) {
 
 }  // namespace
 
+namespace {
+// ------------------------------------------------------------------ LOBPCG
+// NEXT-1 eigensolver variant (opts.method = 1; SURVEY §8(f), P:L2252-2260 for
+// the operator): locally optimal block preconditioned CG on A_r itself, no
+// inner solves, preconditioned by Sigma_r^{-2} (A_r = Sigma_r M Sigma_r, so the
+// preconditioned operator is similar to M, kappa <= max eps / min eps).
+// Knyazev's LOBPCG with soft locking (converged columns stay in the
+// Rayleigh-Ritz basis, only active residuals are preconditioned and applied),
+// X / W / P blocks each orthonormalised by Cholesky-QR, W orthogonalised to X,
+// Rayleigh-Ritz on [X W P] as a generalized Hermitian eigenproblem on the host
+// (P is dropped for one step if its Gram matrix is numerically singular).  A
+// pair is converged when ||A_r x - theta x|| <= res_tol (unit x): the
+// north-star residual bar, which also bounds the eigenvalue error by
+// ||r||^2 / gap.
+int lobpcg_solve(bnf_solver* s, int nev, int want, double* lambda, double& maxres_out, int& iters_out,
+                 bool& converged) {
+    const long long N = 2 * s->nv;
+    const int m = want;
+    const size_t vb = (size_t)N * sizeof(double2);
+    CK(s->lob.ensure(vb * (size_t)m * 10));
+    double2* base = s->lob.as<double2>();
+    double2* X = base;
+    double2* AX = base + (size_t)m * N;
+    double2* W = base + (size_t)2 * m * N;
+    double2* AW = base + (size_t)3 * m * N;
+    double2* P = base + (size_t)4 * m * N;
+    double2* AP = base + (size_t)5 * m * N;
+    double2* T1 = base + (size_t)6 * m * N;
+    double2* T2 = base + (size_t)7 * m * N;
+    double2* T3 = base + (size_t)8 * m * N;
+    double2* T4 = base + (size_t)9 * m * N;
+    CK(s->small.ensure((size_t)(64 + 8 * 3 * m) * sizeof(double2)));
+    // start block: previous Ritz vectors (warm) or seeded normals, Gamma mode masked
+    RUN("fill_random", launch_fill_random(X, N, m, s->o.seed, (long long)s->rank * N * m, s->sigma.as<double>(), s->nv,
+                                          s->st, sig_nloc(s)));
+    if (s->o.warm && s->prev_want > 0) {
+        const int c = std::min(s->prev_want, m);
+        RUN("copy", launch_copy(X, s->Yv.as<double2>(), N * c, s->st));
+        RUN("scale_sigma", launch_scale_sigma(X, X, s->sigma.as<double>(), s->nv, c, 1, s->st, sig_nloc(s)));
+        RUN("scale_sigma", launch_scale_sigma(X, X, s->sigma.as<double>(), s->nv, c, 0, s->st, sig_nloc(s)));
+    }
+    bool ok = true;
+    std::vector<cd> Rq;
+    TRY(chol_qr2(s, X, m, Rq, ok));
+    if (!ok) {
+        set_error("LOBPCG start block rank deficient");
+        return BNF_ENOCONV;
+    }
+    TRY(apply_op(s, X, AX, m, BNF_OP_AR));
+    // Rayleigh-Ritz on X
+    std::vector<double> theta;
+    {
+        std::vector<cd> H, Z;
+        TRY(gram_host(s, X, m, AX, m, H));
+        for (int i = 0; i < m; ++i)
+            for (int j = i; j < m; ++j) {
+                const cd h = 0.5 * (H[(size_t)i * m + j] + std::conj(H[(size_t)j * m + i]));
+                H[(size_t)i * m + j] = h;
+                H[(size_t)j * m + i] = std::conj(h);
+            }
+        herm_eig(m, H, theta, &Z);
+        TRY(gemm_nn_host(s, X, m, Z, m, T1, 1.0, 0.0));
+        TRY(gemm_nn_host(s, AX, m, Z, m, T2, 1.0, 0.0));
+        std::swap(X, T1);
+        std::swap(AX, T2);
+    }
+    const int maxit = s->o.max_outer > 0 ? s->o.max_outer : 1000;
+    bool have_p = false;
+    std::vector<int> pact;   // columns of P / AP that are valid (all m after the first update)
+    double maxres = 0.0;
+    int it = 0;
+    converged = false;
+    double2* dd = s->small.as<double2>();
+    for (; it < maxit; ++it) {
+        // residuals R = AX - X diag(theta) (into T1) and their norms
+        RUN("copy", launch_copy(T1, AX, N * m, s->st));
+        {
+            std::vector<cd> Dl((size_t)m * m, 0.0);
+            for (int c = 0; c < m; ++c) Dl[(size_t)c * m + c] = -theta[c];
+            TRY(gemm_nn_host(s, X, m, Dl, m, T1, 1.0, 1.0));
+        }
+        TRY(dots(s, T1, T1, N, m, dd));
+        std::vector<cd> rr;
+        TRY(get_small(s, dd, m, rr));
+        std::vector<int> act;
+        maxres = 0.0;
+        for (int c = 0; c < m; ++c) {
+            const double r = std::sqrt(std::fabs(rr[c].real()));
+            if (c < nev) maxres = std::max(maxres, r);
+            if (r > s->o.res_tol) act.push_back(c);
+        }
+        bool wanted_done = true;
+        for (int c : act)
+            if (c < nev) wanted_done = false;
+        if (wanted_done) {
+            converged = true;
+            break;
+        }
+        const int k = (int)act.size();
+        // W = T R_active, T = Sigma_r^{-2} (Gamma masked)
+        for (int q = 0; q < k; ++q) RUN("copy", launch_copy(W + (size_t)q * N, T1 + (size_t)act[q] * N, N, s->st));
+        RUN("scale_sigma", launch_scale_sigma(W, W, s->sigma.as<double>(), s->nv, k, 1, s->st, sig_nloc(s)));
+        RUN("scale_sigma", launch_scale_sigma(W, W, s->sigma.as<double>(), s->nv, k, 1, s->st, sig_nloc(s)));
+        // W <- W - X (X^* W), twice; orthonormalise
+        for (int pass = 0; pass < 2; ++pass) {
+            std::vector<cd> Hxw;
+            TRY(gram_host(s, X, m, W, k, Hxw));
+            TRY(gemm_nn_host(s, X, m, Hxw, k, W, -1.0, 1.0));
+        }
+        TRY(chol_qr2(s, W, k, Rq, ok));
+        if (!ok) break;   // stagnation: keep the current Ritz pairs
+        TRY(apply_op(s, W, AW, k, BNF_OP_AR));
+        // P restricted to the active columns, orthonormalised (AP transformed alike)
+        int kp = 0;
+        if (have_p) {
+            for (int q = 0; q < k; ++q) {
+                RUN("copy", launch_copy(T3 + (size_t)q * N, P + (size_t)act[q] * N, N, s->st));
+                RUN("copy", launch_copy(T4 + (size_t)q * N, AP + (size_t)act[q] * N, N, s->st));
+            }
+            std::vector<cd> Rp, Rpi;
+            TRY(chol_qr2(s, T3, k, Rp, ok));
+            if (ok) {
+                inv_upper(k, Rp, Rpi);
+                TRY(gemm_nn_host(s, T4, k, Rpi, k, T2, 1.0, 0.0));
+                RUN("copy", launch_copy(T4, T2, N * k, s->st));
+                kp = k;
+            }
+        }
+        // Gram matrices of S = [X W P] (orthonormal blocks; X^* W = 0)
+        auto assemble = [&](int kpu, std::vector<cd>& GA, std::vector<cd>& GB) -> int {
+            const int sz = m + k + kpu;
+            GA.assign((size_t)sz * sz, 0.0);
+            GB.assign((size_t)sz * sz, 0.0);
+            for (int i = 0; i < sz; ++i) GB[(size_t)i * sz + i] = 1.0;
+            for (int i = 0; i < m; ++i) GA[(size_t)i * sz + i] = theta[i];
+            std::vector<cd> H;
+            auto put = [&](std::vector<cd>& G, int r0, int c0, int pr, int qc, const std::vector<cd>& B) {
+                for (int a = 0; a < pr; ++a)
+                    for (int c = 0; c < qc; ++c) {
+                        G[(size_t)(r0 + a) * sz + c0 + c] = B[(size_t)a * qc + c];
+                        G[(size_t)(c0 + c) * sz + r0 + a] = std::conj(B[(size_t)a * qc + c]);
+                    }
+            };
+            TRY(gram_host(s, X, m, AW, k, H));
+            put(GA, 0, m, m, k, H);
+            TRY(gram_host(s, W, k, AW, k, H));
+            for (int a = 0; a < k; ++a)
+                for (int c = a; c < k; ++c) {
+                    const cd h = 0.5 * (H[(size_t)a * k + c] + std::conj(H[(size_t)c * k + a]));
+                    GA[(size_t)(m + a) * sz + m + c] = h;
+                    GA[(size_t)(m + c) * sz + m + a] = std::conj(h);
+                }
+            if (kpu > 0) {
+                TRY(gram_host(s, X, m, T4, kpu, H));
+                put(GA, 0, m + k, m, kpu, H);
+                TRY(gram_host(s, W, k, T4, kpu, H));
+                put(GA, m, m + k, k, kpu, H);
+                TRY(gram_host(s, T3, kpu, T4, kpu, H));
+                for (int a = 0; a < kpu; ++a)
+                    for (int c = a; c < kpu; ++c) {
+                        const cd h = 0.5 * (H[(size_t)a * kpu + c] + std::conj(H[(size_t)c * kpu + a]));
+                        GA[(size_t)(m + k + a) * sz + m + k + c] = h;
+                        GA[(size_t)(m + k + c) * sz + m + k + a] = std::conj(h);
+                    }
+                TRY(gram_host(s, X, m, T3, kpu, H));
+                put(GB, 0, m + k, m, kpu, H);
+                TRY(gram_host(s, W, k, T3, kpu, H));
+                put(GB, m, m + k, k, kpu, H);
+            }
+            return BNF_OK;
+        };
+        std::vector<cd> GA, GB, RB, RBi;
+        TRY(assemble(kp, GA, GB));
+        int sz = m + k + kp;
+        if (!cholesky_upper(sz, GB, RB)) {   // P numerically dependent: Rayleigh-Ritz on [X W] only
+            kp = 0;
+            TRY(assemble(0, GA, GB));
+            sz = m + k;
+            if (!cholesky_upper(sz, GB, RB)) break;
+        }
+        inv_upper(sz, RB, RBi);
+        // standard form RB^{-H} GA RB^{-1}
+        std::vector<cd> T((size_t)sz * sz, 0.0), A2((size_t)sz * sz, 0.0);
+        for (int i = 0; i < sz; ++i)
+            for (int j = 0; j < sz; ++j) {
+                cd acc = 0.0;
+                for (int l = 0; l <= j; ++l) acc += GA[(size_t)i * sz + l] * RBi[(size_t)l * sz + j];
+                T[(size_t)i * sz + j] = acc;
+            }
+        for (int i = 0; i < sz; ++i)
+            for (int j = 0; j < sz; ++j) {
+                cd acc = 0.0;
+                for (int l = 0; l <= i; ++l) acc += std::conj(RBi[(size_t)l * sz + i]) * T[(size_t)l * sz + j];
+                A2[(size_t)i * sz + j] = acc;
+            }
+        for (int i = 0; i < sz; ++i)
+            for (int j = i; j < sz; ++j) {
+                const cd h = 0.5 * (A2[(size_t)i * sz + j] + std::conj(A2[(size_t)j * sz + i]));
+                A2[(size_t)i * sz + j] = h;
+                A2[(size_t)j * sz + i] = std::conj(h);
+            }
+        std::vector<double> w;
+        std::vector<cd> Z;
+        herm_eig(sz, A2, w, &Z);
+        // C = RB^{-1} Z[:, :m]
+        std::vector<cd> Cx((size_t)m * m), Cw((size_t)k * m), Cp((size_t)std::max(kp, 1) * m);
+        for (int i = 0; i < sz; ++i)
+            for (int c = 0; c < m; ++c) {
+                cd acc = 0.0;
+                for (int l = i; l < sz; ++l) acc += RBi[(size_t)i * sz + l] * Z[(size_t)l * sz + c];
+                if (i < m) Cx[(size_t)i * m + c] = acc;
+                else if (i < m + k) Cw[(size_t)(i - m) * m + c] = acc;
+                else Cp[(size_t)(i - m - k) * m + c] = acc;
+            }
+        // P_new = W Cw + P Cp; AP_new = AW Cw + AP Cp (into T1 / T2, then into P / AP)
+        TRY(gemm_nn_host(s, W, k, Cw, m, T1, 1.0, 0.0));
+        TRY(gemm_nn_host(s, AW, k, Cw, m, T2, 1.0, 0.0));
+        if (kp > 0) {
+            TRY(gemm_nn_host(s, T3, kp, Cp, m, T1, 1.0, 1.0));
+            TRY(gemm_nn_host(s, T4, kp, Cp, m, T2, 1.0, 1.0));
+        }
+        // X_new = X Cx + P_new; AX_new = AX Cx + AP_new
+        TRY(gemm_nn_host(s, X, m, Cx, m, T3, 1.0, 0.0));
+        TRY(gemm_nn_host(s, AX, m, Cx, m, T4, 1.0, 0.0));
+        RUN("copy", launch_copy(P, T1, N * m, s->st));
+        RUN("copy", launch_copy(AP, T2, N * m, s->st));
+        std::swap(X, T3);
+        std::swap(AX, T4);
+        // X += P_new, AX += AP_new  (beta-accumulate through an identity product)
+        {
+            std::vector<cd> I((size_t)m * m, 0.0);
+            for (int c = 0; c < m; ++c) I[(size_t)c * m + c] = 1.0;
+            TRY(gemm_nn_host(s, P, m, I, m, X, 1.0, 1.0));
+            TRY(gemm_nn_host(s, AP, m, I, m, AX, 1.0, 1.0));
+        }
+        theta.assign(w.begin(), w.begin() + m);
+        have_p = true;
+    }
+    // final Ritz pairs: Y = X (unit columns), lambda = theta
+    CK(s->Yv.ensure(vb * want));
+    RUN("copy", launch_copy(s->Yv.as<double2>(), X, N * want, s->st));
+    for (int c = 0; c < nev; ++c) lambda[c] = theta[c];
+    s->lam.assign(theta.begin(), theta.begin() + nev);
+    maxres_out = maxres;
+    iters_out = it;
+    return BNF_OK;
+}
+}  // namespace
+
 // ======================================================================= C ABI
 extern "C" {
 
@@ -1258,6 +1508,7 @@ void bnf_opts_default(bnf_opts* o) {
     o->max_polish = 3;
     o->slabs = 1;
     o->relax_inner = 0;
+    o->method = 0;
 }
 
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out) {
@@ -1676,6 +1927,33 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     if (want > dof) {
         set_error("nev + guard exceeds the NFSEP dimension");
         return BNF_EINVAL;
+    }
+    if (s->o.method == 1) {   // NEXT-1: LOBPCG on A_r, preconditioned by Sigma_r^{-2}
+        double maxres = 0.0;
+        int iters = 0;
+        bool conv = false;
+        TRY(lobpcg_solve(s, nev, want, lambda, maxres, iters, conv));
+        s->nev_last = nev;
+        s->prev_want = want;
+        CK(cudaStreamSynchronize(s->st));
+        if (s->prof.on) s->prof.flush();
+        if (stats) {
+            stats->outer_steps = iters;
+            stats->converged = conv ? 1 : 0;
+            stats->inner_iters = 0;
+            stats->matvecs = s->matvecs;
+            stats->kernel_launches = s->prof.launches - launches0;
+            stats->max_ritz_residual = maxres;
+            stats->max_residual = maxres;
+            stats->polish_steps = 0;
+            stats->polish_failed = 0;
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        if (!conv) {
+            set_error("LOBPCG did not reach res_tol within max_outer iterations");
+            return BNF_ENOCONV;
+        }
+        return BNF_OK;
     }
     // Lanczos step cap: opts.max_outer, or (0 = auto) enough steps for the wanted
     // pairs with a margin that scales with ceil(want / b) -- single-vector runs

@@ -719,3 +719,19 @@ def test_relaxed_inner_tolerance_same_eigenvalues(bnf):
     _, _, _, S0 = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape)
     lam0, st0 = S0.solve(tuple(g["kappa"]), len(g["lambda"]))
     assert st["matvecs"] < st0["matvecs"], (st["matvecs"], st0["matvecs"])
+
+
+@pytest.mark.parametrize("fname", ["full_c2_k9_oracle.json", "full_c4_k12_oracle.json"])
+def test_lobpcg_matches_golden(bnf, golden_dir, fname):
+    """NEXT-1 LOBPCG (bnf_opts.method = 1: A_r preconditioned by Sigma_r^{-2},
+    no inner solves) returns the oracle golden eigenvalues to 1e-10 with every
+    pair at the north-star residual, at 64^3 (config 2) and 128^3 (config 4)."""
+    path = os.path.join(golden_dir, fname)
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    g = _golden(golden_dir, fname)
+    cfg = configs.config(g["config"])
+    L, O, eps, S = _setup(bnf, cfg.a_raw, tuple(g["n"]), cfg.shape, method=1, guard=4)
+    lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
+    assert st["converged"] == 1 and st["max_residual"] <= 5e-9
+    np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
