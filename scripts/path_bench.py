@@ -41,6 +41,9 @@ def main():
     ap.add_argument("--warm", type=int, default=1)
     ap.add_argument("--per-gpu", type=int, default=1, help="concurrent solvers (streams) per GPU")
     ap.add_argument("--relax-inner", type=int, default=0)
+    ap.add_argument("--method", type=int, default=0, help="0 inverse Lanczos (paper), 1 LOBPCG (NEXT-1)")
+    ap.add_argument("--kmax", type=int, default=0, help="only the first kmax k-points of each path")
+    ap.add_argument("--guard", type=int, default=None)
     a = ap.parse_args()
     gold = goldens()
     res = []
@@ -49,10 +52,13 @@ def main():
         lat = bnf.Lattice(cfg.a_raw, cfg.n)
         eps = eps_for(cfg, lat)
         ks = kappas(cfg, lat)
+        if a.kmax:
+            ks = ks[:a.kmax]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        extra = {"guard": a.guard} if a.guard is not None else {}
         recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=a.per_gpu,
-                                relax_inner=a.relax_inner)
+                                relax_inner=a.relax_inner, method=a.method, **extra)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         dev = []
@@ -62,7 +68,7 @@ def main():
                 g = np.asarray(gold[key][:len(r.lam)])
                 dev.append(float(np.max(np.abs(np.asarray(r.lam[:len(g)]) - g) / g)))
         line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
-                "per_gpu": a.per_gpu, "relax_inner": a.relax_inner,
+                "per_gpu": a.per_gpu, "relax_inner": a.relax_inner, "method": a.method,
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "matvecs_per_kpoint": float(np.mean([r.stats["matvecs"] for r in recs])),
                 "max_residual": max(r.stats["max_residual"] for r in recs),
