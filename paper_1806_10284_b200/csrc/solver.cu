@@ -1209,10 +1209,13 @@ int lobpcg_solve(bnf_solver* s, int nev, int want, double* lambda, double& maxre
         TRY(get_small(s, dd, m, rr));
         std::vector<int> act;
         maxres = 0.0;
+        // converged: ||r|| <= min(res_tol, 2e-11 theta): the Bauer-Fike bound |lambda - theta| <= ||r||
+        // then keeps every returned eigenvalue within 2e-11 relative (clustered bands leave no room for
+        // the quadratic ||r||^2 / gap bound), and the north-star residual bar holds
         for (int c = 0; c < m; ++c) {
             const double r = std::sqrt(std::fabs(rr[c].real()));
             if (c < nev) maxres = std::max(maxres, r);
-            if (r > s->o.res_tol) act.push_back(c);
+            if (r > std::min(s->o.res_tol, 2e-11 * std::fabs(theta[c]))) act.push_back(c);
         }
         bool wanted_done = true;
         for (int c : act)
