@@ -235,6 +235,24 @@ def gather(records, nk, group=None):
     return merge([[KRecord.from_json(x) for x in p] for p in allp], nk)
 
 
+def band_gaps(records, nbands=None):
+    """Complete band gaps of a path (NEXT-2): for each pair of
+    consecutive bands (i, i+1), gap_i = min_k omega_{i+1}(k) - max_k omega_i(k)
+    in omega / (2 pi) units.  Returns a list of (i, lower edge,
+    upper edge, width, width / midgap) for the positive gaps, widest first."""
+    om = [frequencies(r.lam if hasattr(r, "lam") else r) for r in records if r is not None]
+    if not om:
+        return []
+    nb = min(len(o) for o in om) if nbands is None else nbands
+    out = []
+    for i in range(nb - 1):
+        lo = max(o[i] for o in om)
+        hi = min(o[i + 1] for o in om)
+        if hi > lo:
+            out.append((i, lo, hi, hi - lo, 2.0 * (hi - lo) / (hi + lo)))
+    return sorted(out, key=lambda g: -g[3])
+
+
 def frequencies(lam):
     """omega / (2 pi) = sqrt(lambda) / (2 pi) (band-plot convention)."""
     return [math.sqrt(max(x, 0.0)) / (2.0 * math.pi) for x in lam]

@@ -15,6 +15,10 @@ Recipes:
                   neighbours (a/4)(1,1,1),(1,-1,-1),(-1,1,-1),(-1,-1,1)
   bcc_sphere_rod  eps=13 spheres r=0.3 at lattice points + rods r=0.1 along
                   a1, a2, a3, a1+a2+a3 (the 4 nearest-neighbour bonds)
+  gyroid[:<eps>]  eps (default 16) where the single-gyroid level set
+                  sin(2 pi x/a) cos(2 pi y/a) + sin(2 pi y/a) cos(2 pi z/a)
+                  + sin(2 pi z/a) cos(2 pi x/a) > 1.1, else 1 (PAPER.md
+                  L2402-2407; BCC lattice; periodic under (a/2)(1,1,1))
   noise42         seed-42 Gaussian cell field smoothed (sigma=2 cells),
                   edge value = mean of its two endpoint cells, thresholded at
                   the median of the cell field -> eps in {1, 12}
@@ -52,8 +56,17 @@ def _seg_dist2(X, p0, p1):
     return np.einsum("ij,ij->i", r, r)
 
 
+def gyroid_level(X, a=1.0):
+    """The gyroid level-set function of PAPER.md L2404-2405 at Cartesian points X (m, 3)."""
+    u = 2.0 * np.pi * np.asarray(X, dtype=np.float64) / a
+    return (np.sin(u[:, 0]) * np.cos(u[:, 1]) + np.sin(u[:, 1]) * np.cos(u[:, 2]) +
+            np.sin(u[:, 2]) * np.cos(u[:, 0]))
+
+
 def _inside(X, shape, a_orig):
     """X: (m,3) points in the original frame reduced into the primitive cell."""
+    if shape == "gyroid":
+        return gyroid_level(X) > 1.1
     imgs = _images(a_orig)
     inside = np.zeros(X.shape[0], dtype=bool)
     if shape == "sc_sphere":
@@ -75,7 +88,7 @@ def _inside(X, shape, a_orig):
     return inside
 
 
-def _geometric(shape, a_snap, delta, n, a_orig, chunk=1 << 18):
+def _geometric(shape, a_snap, delta, n, a_orig, chunk=1 << 18, eps_in=EPS_IN):
     inv = np.linalg.inv(np.asarray(a_snap, dtype=np.float64))
     out = []
     for comp in range(3):
@@ -85,7 +98,7 @@ def _geometric(shape, a_snap, delta, n, a_orig, chunk=1 << 18):
             f = x[s:s + chunk] @ inv.T
             f -= np.floor(f)
             X = f @ np.asarray(a_orig, dtype=np.float64).T
-            e[s:s + chunk] = np.where(_inside(X, shape, a_orig), EPS_IN, EPS_OUT)
+            e[s:s + chunk] = np.where(_inside(X, shape, a_orig), eps_in, EPS_OUT)
         out.append(e.reshape(n[2], n[1], n[0]))
     return out
 
@@ -118,6 +131,9 @@ def sample(shape, n, a_snap=None, delta=None, a_orig=None):
         seed = int(shape.split(":")[1]) if ":" in shape else 0
         rng = np.random.default_rng(seed)
         return [1.0 + 12.0 * rng.random((n[2], n[1], n[0])) for _ in range(3)]
+    if shape.startswith("gyroid"):
+        eps_in = float(shape.split(":")[1]) if ":" in shape else 16.0
+        return _geometric("gyroid", a_snap, delta, n, a_orig, eps_in=eps_in)
     return _geometric(shape, a_snap, delta, n, a_orig)
 
 

@@ -735,3 +735,16 @@ def test_lobpcg_matches_golden(bnf, golden_dir, fname):
     lam, st = S.solve(tuple(g["kappa"]), len(g["lambda"]))
     assert st["converged"] == 1 and st["max_residual"] <= 5e-9
     np.testing.assert_allclose(lam, g["lambda"], rtol=1e-10)
+
+
+def test_gyroid_bcc_vs_dense_oracle(bnf):
+    """NEXT-2 workload on a small grid: the gyroid BCC crystal (PAPER.md
+    L2402-2407, eps = 16) at the H point: GPU eigenvalues equal the dense
+    NFSEP oracle (plain definition) to 1e-10."""
+    a = configs.bcc_vectors()
+    n = (8, 8, 8)
+    L, O, eps, S = _setup(bnf, a, n, "gyroid:16")
+    kap = (0.5, -0.5, 0.5)
+    dense = np.linalg.eigvalsh(spectral.Ar_dense(O, kap, eps))[:8]
+    lam, _ = S.solve(kap, 8)
+    np.testing.assert_allclose(lam, dense, rtol=1e-10)

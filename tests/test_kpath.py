@@ -191,3 +191,14 @@ def test_work_stealing_world2_gloo():
     single = kpath.merge([kpath.run_path(_fake_solve, kaps, range(len(kaps)))], len(kaps))
     for m, s in zip(merged, single):
         assert m[2] == s.lam
+
+
+def test_band_gaps():
+    """NEXT-2 gap extraction: bands given as lambda = (2 pi omega)^2; a gap
+    between bands 1 and 2 (0-based) of width 0.1 in omega / (2 pi)."""
+    import math
+    om = [[0.25, 0.3, 0.5], [0.15, 0.2, 0.45], [0.12, 0.28, 0.4]]
+    recs = [[(2 * math.pi * w) ** 2 for w in o] for o in om]
+    g = kpath.band_gaps(recs)
+    assert len(g) == 1 and g[0][0] == 1
+    assert abs(g[0][1] - 0.3) < 1e-12 and abs(g[0][2] - 0.4) < 1e-12 and abs(g[0][3] - 0.1) < 1e-12

@@ -121,3 +121,28 @@ def test_canonical_relabel_and_rejects():
     assert L.sign3 == -1
     with pytest.raises(ValueError):
         lattice.snap(configs.sc_vectors(), (0, 4, 4))
+
+
+def test_gyroid_sampling_bcc():
+    """NEXT-2 input: the gyroid of PAPER.md L2402-2407 sampled on the BCC cell
+    equals the level set evaluated directly at the Yee points (mapped to the
+    original frame), is invariant under the BCC translation (a/2)(1,1,1), and
+    fills a plausible fraction of the cell."""
+    from synthetic import configs
+    from synthetic import eps as E
+    a = configs.bcc_vectors()
+    n = (12, 12, 12)
+    L = lattice.snap(a, n)
+    ep = E.sample("gyroid:16", n, L.a, L.delta, L.a_canon)
+    inv = np.linalg.inv(L.a)
+    for comp in range(3):
+        x = E.yee_points(L.delta, n, comp)
+        f = x @ inv.T
+        f -= np.floor(f)
+        X = f @ L.a_canon.T
+        want = np.where(E.gyroid_level(X) > 1.1, 16.0, 1.0)
+        assert np.array_equal(ep[comp].ravel(), want)
+        shifted = E.gyroid_level(X + 0.5)
+        np.testing.assert_allclose(shifted, E.gyroid_level(X), atol=1e-12)
+    frac = np.mean(np.concatenate([e.ravel() for e in ep]) > 1.0)
+    assert 0.02 < frac < 0.3, frac
