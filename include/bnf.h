@@ -189,8 +189,10 @@ typedef struct {
 } bnf_stats;
 
 /* Create a solver for a lattice on opts->device.  Allocates device memory
-   for the operator work arrays.  BNF_EINVAL if an axis length has a prime
-   factor > 31 or exceeds 1024. */
+   for the operator work arrays.  Any axis length up to 1024: lengths with a
+   register-FFT plan (8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256) take the
+   fused fast path, the others generic Stockham passes (a prime factor > 31 is
+   evaluated as a direct DFT stage).  BNF_EINVAL beyond 1024. */
 int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver** out);
 void bnf_solver_destroy(bnf_solver* s);
 

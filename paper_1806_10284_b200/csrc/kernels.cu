@@ -123,10 +123,33 @@ __device__ __forceinline__ void stage_fixed(const double2* __restrict__ A, doubl
     for (int r = 0; r < R; ++r) B[(base + r * Ns) * ld + col] = v[r];
 }
 
+// Radix R > 32 (a large prime factor of an awkward axis length; NEXT-4): the
+// R-point DFT of the stage evaluated directly from shared memory, O(R^2) per
+// R outputs -- correct for any factor, meant for the occasional prime such
+// as 37 or 41, not for speed.
+template <int SIGN>
+__device__ void stage_direct(int R, int N, const double2* __restrict__ A, double2* __restrict__ B, int ld, int col,
+                             int j, int nb, int k, int tstride, int base, int Ns, const double2* __restrict__ root) {
+    const int step = N / R;
+    for (int s = 0; s < R; ++s) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int r = 0; r < R; ++r) {
+            double2 x = A[(j + r * nb) * ld + col];
+            if (Ns > 1 && r > 0) x = cmul(x, root_tw<SIGN>(root, k * r * tstride));
+            acc = cadd(acc, cmul(x, root_tw<SIGN>(root, ((r * s) % R) * step)));
+        }
+        B[(base + s * Ns) * ld + col] = acc;
+    }
+}
+
 template <int SIGN>
 __device__ void stage_generic(int R, int N, const double2* __restrict__ A, double2* __restrict__ B, int ld, int col,
                               int j, int nb, int k, int tstride, int base, int Ns,
                               const double2* __restrict__ root) {
+    if (R > 32) {
+        stage_direct<SIGN>(R, N, A, B, ld, col, j, nb, k, tstride, base, Ns, root);
+        return;
+    }
     double2 v[32];
     for (int r = 0; r < R; ++r) {
         double2 x = A[(j + r * nb) * ld + col];

@@ -76,7 +76,7 @@ bool make_plan(int N, std::vector<int>& radices) {
         radices.push_back(3);
         m /= 3;
     }
-    for (int p = 5; m > 1 && p <= 31; p += 2) {
+    for (int p = 5; m > 1 && p <= 1024; p += 2) {   // factors > 31: direct-DFT stage (kernels.cu stage_direct)
         while (m % p == 0) {
             radices.push_back(p);
             m /= p;
@@ -1548,7 +1548,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     for (int d = 0; d < 3; ++d) {
         std::vector<int> rad;
         if (!make_plan(L.n[d], rad)) {
-            set_error("axis length " + std::to_string(L.n[d]) + " unsupported (need <= 1024, prime factors <= 31)");
+            set_error("axis length " + std::to_string(L.n[d]) + " unsupported (need 1 <= length <= 1024)");
             return BNF_EINVAL;
         }
         AxisPlan& pl = *plans[d];

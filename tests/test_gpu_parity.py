@@ -141,10 +141,27 @@ def test_batch_equals_single(bnf):
 
 
 def test_unsupported_axis_rejected(bnf):
-    L = bnf.Lattice(configs.sc_vectors(), (37, 8, 8))
+    L = bnf.Lattice(configs.sc_vectors(), (1031, 2, 2))
     with pytest.raises(bnf.BnfError) as e:
         bnf.Solver(L)
     assert e.value.code == bnf.EINVAL
+
+
+def test_large_prime_axes_vs_dense_oracle(bnf):
+    """NEXT-4 awkward grids: axis lengths with prime factors > 31 (37, 41 x 2)
+    run the direct-DFT stage of the generic passes; A_r vs the dense oracle and
+    a solve vs dense eigh."""
+    a = configs.triclinic_vectors(1.0, 0.9, 0.8, 70, 100, 110)
+    for n in ((37, 4, 3), (3, 82, 2)):
+        L, O, eps, S = _setup(bnf, a, n, "random:9")
+        kap = (0.17, -0.29, 0.33)
+        D = spectral.Ar_dense(O, kap, eps)
+        y = vectors.complex_normal((2, 2 * O.nn), seed=5)
+        got = _apply_gpu(S, kap, y, bnf.OP_AR)
+        want = y @ D.T
+        assert np.abs(got - want).max() <= OP_TOL * np.abs(want).max(), n
+        lam, _ = S.solve(kap, 6)
+        np.testing.assert_allclose(lam, np.linalg.eigvalsh(D)[:6], rtol=1e-10)
 
 
 # ------------------------------------------------------------- eigensolver
