@@ -168,7 +168,8 @@ typedef struct {
     int method;                 /* eigensolver: 0 (default) = the paper's inverse Lanczos with CG inner
                                    solves; 1 = NEXT-1 LOBPCG on A_r preconditioned by
                                    Sigma_r^{-2} (no inner solves; block nev + guard, soft locking),
-                                   stopping at ||A_r y - lambda y|| <= min(res_tol, 2e-11 lambda); max_outer = iteration
+                                   stopping at ||A_r y - lambda y|| <= min(res_tol, 1e-9 max(1, lambda)),
+                                   falling back to method 0 on stagnation or breakdown; max_outer = iteration
                                    cap (0: 1000); block / tol_outer / tol_inner are not used. */
 } bnf_opts;
 

@@ -61,6 +61,10 @@ def main():
                                 relax_inner=a.relax_inner, method=a.method, **extra)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        failed = [(r.index, r.stats.get("error")) for r in recs if r.status == "failed"]
+        for f in failed:
+            print("FAILED k %d: %s" % f, flush=True)
+        recs = [r for r in recs if r.status != "failed"] or recs
         dev = []
         for r in recs:
             key = (idx, tuple(round(x, 12) for x in r.kappa))
@@ -70,9 +74,10 @@ def main():
         line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
                 "per_gpu": a.per_gpu, "relax_inner": a.relax_inner, "method": a.method,
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
-                "matvecs_per_kpoint": float(np.mean([r.stats["matvecs"] for r in recs])),
-                "max_residual": max(r.stats["max_residual"] for r in recs),
-                "residual_per_k": [float("%.3g" % r.stats["max_residual"]) for r in recs],
+                "failed_kpoints": failed,
+                "matvecs_per_kpoint": float(np.mean([r.stats.get("matvecs", 0) for r in recs])),
+                "max_residual": max(r.stats.get("max_residual", float("nan")) for r in recs),
+                "residual_per_k": [float("%.3g" % r.stats.get("max_residual", float("nan"))) for r in recs],
                 "polish_steps_per_k": [int(r.stats.get("polish_steps", 0)) for r in recs],
                 "golden_kpoints": len(dev), "max_rel_dev_vs_oracle": max(dev) if dev else None,
                 "lambda_first_k": recs[0].lam[:4], "omega_over_2pi_first_k": kpath.frequencies(recs[0].lam[:4])}
