@@ -187,6 +187,9 @@ typedef struct {
     int polish_steps;           /* extra inverse-iteration + Rayleigh-Ritz steps taken for res_tol */
     int polish_failed;          /* 1 if a polish step's block was rank deficient (CholQR failed): the
                                    previous Ritz pairs were kept and polishing stopped */
+    long long active_matvecs;   /* the part of matvecs applied to right-hand sides still iterating: a block
+                                   CG keeps applying M to its converged columns until the last one stops
+                                   (matvecs - active_matvecs is that overhead) */
 } bnf_stats;
 
 /* Create a solver for a lattice on opts->device.  Allocates device memory

@@ -52,7 +52,8 @@ class Stats(C.Structure):
     _fields_ = [("outer_steps", C.c_int), ("converged", C.c_int), ("inner_iters", C.c_longlong),
                 ("matvecs", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("max_ritz_residual", C.c_double), ("max_residual", C.c_double), ("seconds", C.c_double),
-                ("polish_steps", C.c_int), ("polish_failed", C.c_int)]
+                ("polish_steps", C.c_int), ("polish_failed", C.c_int),
+                ("active_matvecs", C.c_longlong)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -62,6 +62,7 @@ __device__ __forceinline__ void cg_alpha_update(const CGFuse& cg, int v, double 
 }
 __device__ __forceinline__ void cg_beta_update(const CGFuse& cg, int v, double rn) {
     const int act = cg.active[v];
+    if (act && cg.iter != nullptr) atomicAdd(cg.iter + 3, 1);   // applications to a still-iterating vector
     cg.beta[v] = (act && cg.rr[v] > 0.0) ? rn / cg.rr[v] : 0.0;
     if (act) cg.rr[v] = rn;
     cg.active[v] = (act && rn > cg.thr[v]) ? 1 : 0;

@@ -20,6 +20,9 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "cgfuse.cuh"
 #include "fastfft.cuh"
@@ -1236,10 +1239,28 @@ bool has_fast(int N) {
     }
 }
 
+}  // namespace
+
+cudaError_t allow_smem(const void* f, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> granted;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& g = granted[{f, dev}];
+    if (bytes <= g) return cudaSuccess;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) g = bytes;
+    return e;
+}
+
+namespace {
+
 template <class F, class... Args>
 cudaError_t launch_k(F f, dim3 g, int threads, size_t sm, cudaStream_t st, Args... args) {
     if (sm > 32 * 1024) {   // leave room for the kernels' static shared memory
-        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = allow_smem((const void*)f, sm);
         if (e != cudaSuccess) return e;
     }
     f<<<g, threads, sm, st>>>(args...);
@@ -1320,8 +1341,7 @@ static size_t smem_y(const OpArgs& a) { return (size_t)2 * a.mp.n2 * a.W_y * siz
 static size_t smem_x(const OpArgs& a) { return (size_t)2 * a.mp.n1 * (a.R_x + 1) * sizeof(double2); }
 
 static cudaError_t set_smem(const void* f, size_t bytes) {
-    if (bytes > 32 * 1024) return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    return cudaSuccess;
+    return bytes > 32 * 1024 ? allow_smem(f, bytes) : cudaSuccess;
 }
 
 cudaError_t launch_zfwd(const OpArgs& a, const double2* Y, double2* U, int nvec, int op, cudaStream_t st) {

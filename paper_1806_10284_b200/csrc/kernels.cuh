@@ -122,6 +122,11 @@ size_t cg_partials_per_vec(const OpArgs& a);
 // x-DFT*, twiddle*, y-DFT* on every (component, z-plane) of nslab = 3*nvec
 // component slabs, one HBM read + write.  Square xy planes with a fast plan.
 bool plane_supported(const OpArgs& a);
+// Raise kernel f's dynamic shared memory limit (cudaFuncAttributeMaxDynamicSharedMemorySize) to at
+// least `bytes` on the current device.  The attribute is process-wide per function, so it only ever
+// grows (under a lock): concurrent solvers (kpath per_gpu > 1) launching the same kernel with
+// different sizes cannot lower it under one another's launch.
+cudaError_t allow_smem(const void* f, size_t bytes);
 bool plane_w_supported(const OpArgs& a);
 // TMA-staged plane pass (plane_tma.cu): one slab, square 64/128/256 planes.  The
 // tensor maps describe the plane buffer as [planes][N][2N doubles] (plane_t_encode).

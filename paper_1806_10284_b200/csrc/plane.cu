@@ -553,7 +553,7 @@ cudaError_t launch_plane_w_t(const OpArgs& a, double2* U, int nslab, const CGFus
     using C = PlaneWCfg<N1, N2, NWARP, XSHFL>;
     const dim3 g((unsigned)a.n3loc, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+        cudaError_t e = allow_smem((const void*)kern, C::smem);
         if (e != cudaSuccess) return e;
         kern<<<g, C::NT, C::smem, st>>>(U, a, cgarg);
         return cudaGetLastError();
@@ -573,7 +573,7 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
     const size_t smem = (size_t)C::SMEM * sizeof(double2) + (EPF ? (size_t)C::N * C::N : 0) + 256 * sizeof(double);
     const dim3 g((unsigned)a.n3loc, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
         kern<<<g, C::NT, smem, st>>>(U, a, cgarg);
         return cudaGetLastError();
@@ -603,7 +603,7 @@ cudaError_t launch_plane_t(const OpArgs& a, double2* U, int nslab, const CGFuse*
     cfg.numAttrs = 1;
     const int total = a.n3loc * nslab;
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
         if (P > 8) {
             e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

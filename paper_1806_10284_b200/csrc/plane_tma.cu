@@ -340,7 +340,7 @@ cudaError_t launch_plane_t_t(const OpArgs& a, int nslab, const CGFuse* cg, cudaS
                              const CUtensorMap& mx, int zbase) {
     const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg, size_t smem, int nt) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
         kern<<<g, nt, smem, st>>>(a, cgarg, my, mx, zbase);
         return cudaGetLastError();

@@ -376,7 +376,8 @@ struct bnf_solver {
     cudaStream_t cap = nullptr;   // capture stream
     long long kver = 0;           // bumped whenever OpArgs change (kappa, eps)
     DevBuf phasebuf;              // per-phase cycle counters (BNF_PHASE_PROF)
-    DevBuf iterbuf;               // int[3]: per-call CG iterations, total iterations, total vector-iterations
+    DevBuf iterbuf;               // int[4]: per-call CG iterations, total iterations, total vector-iterations,
+                                  // vector-iterations of still-active vectors ([4], [5]: CG partial counts)
     int* d_iter = nullptr;
     int graph_kernels_per_iter = 0;
     long long graph_calls = 0;
@@ -407,6 +408,7 @@ struct bnf_solver {
     Profiler prof;
     long long matvecs = 0;
     long long inner_iters = 0;
+    long long active_mv = 0;      // CG applications to vectors not yet converged (host-counted part)
 
     ~bnf_solver() {
         if (comm) Nccl::get().commDestroy(comm);
@@ -726,6 +728,16 @@ int gemm_tn(bnf_solver* s, const double2* X, int p, const double2* Y, int q, lon
 }
 
 // ------------------------------------------------------------------ CG
+// number of right-hand sides still iterating (device flags; synchronises the stream)
+static int active_count(bnf_solver* s, int nvec) {
+    if (cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st) != cudaSuccess ||
+        cudaStreamSynchronize(s->st) != cudaSuccess)
+        return nvec;   // the caller's next CK reports the error
+    int act = 0;
+    for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
+    return act;
+}
+
 // Solve M X = C for nvec right-hand sides: plain CG, no
 // preconditioner, per-column stopping ||r|| <= tol ||c||.
 int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_out) {
@@ -744,18 +756,18 @@ int cg_solve(bnf_solver* s, const double2* C, double2* X, int nvec, int* iters_o
     TRY(dots(s, R, R, N, nvec, dd));
     RUN("cg_init", launch_cg_init(s->cgs, dd, nvec, s->tol_inner_eff > 0.0 ? s->tol_inner_eff : s->o.tol_inner, s->st));
     int it = 0;
+    int act_prev = active_count(s, nvec);
     for (; it < s->o.max_inner; ++it) {
         TRY(apply_op(s, P, MP, nvec, BNF_OP_M));
+        s->active_mv += act_prev;
         TRY(dots(s, P, MP, N, nvec, s->cgs.pMp));
         RUN("cg_xr", launch_cg_xr(X, R, P, MP, s->cgs, N, nvec, s->partial.as<double2>(), s->nblk, s->st));
         RUN("dot_final", launch_dot_final(s->partial.as<double2>(), s->nblk, nvec, dd, s->st));
         RUN("cg_scalars", launch_cg_scalars(s->cgs, dd, nvec, s->st));
         RUN("cg_p", launch_cg_p(P, R, s->cgs, N, nvec, s->st));
-        CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
-        CK(cudaStreamSynchronize(s->st));
+        const int act = active_count(s, nvec);
+        act_prev = act;
         if (s->prof.on) s->prof.flush();
-        int act = 0;
-        for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
         if (act == 0) {
             ++it;
             break;
@@ -919,7 +931,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     cg.nb_z = s->d_iter + 5;
     int it = 0;
     if (!s->prof.on && s->use_graph) {
-        cg.iter = s->d_iter;
+        cg.iter = s->d_iter;   // [3] counts the applications to still-active vectors on the device
         cg.max_iter = s->o.max_inner;
         CK(cudaMemsetAsync(s->d_iter, 0, sizeof(int), s->st));   // per-call counter; [1], [2] run on
         cudaGraphExec_t exec = nullptr;
@@ -930,6 +942,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
         s->graph_calls++;
     } else {
         cg.iter = nullptr;
+        int act_prev = active_count(s, nvec);
         for (; it < s->o.max_inner; ++it) {
             // eager: one timed launch per pass (profiling, bnf_kernel_times)
             if (s->nsl > 1 || s->dist) {
@@ -953,11 +966,10 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             RUN("cg_beta", launch_cg_finish(cg, 1, nvec, s->st));
             }
             s->matvecs += nvec;
-            CK(cudaMemcpyAsync(s->h_flags, s->cgs.active, sizeof(int) * nvec, cudaMemcpyDeviceToHost, s->st));
-            CK(cudaStreamSynchronize(s->st));
+            s->active_mv += act_prev;
+            const int act = active_count(s, nvec);
+            act_prev = act;
             if (s->prof.on) s->prof.flush();
-            int act = 0;
-            for (int v = 0; v < nvec; ++v) act += s->h_flags[v];
             if (act == 0) {
                 ++it;
                 break;
@@ -1892,7 +1904,7 @@ int bnf_cg_solve(bnf_solver* s, const void* c, void* x, int b, int max_iter, int
     s->o.max_inner = max_iter;
     s->kver++;   // cached CG graphs carry the iteration cap
     int it = -1;
-    CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
+    CK(cudaMemsetAsync(s->d_iter, 0, 4 * sizeof(int), s->st));
     const long long g0 = s->graph_calls;
     const int rc = s->fused_ok ? cg_solve_fused(s, (const double2*)c, (double2*)x, b, &it)
                                : cg_solve(s, (const double2*)c, (double2*)x, b, &it);
@@ -1923,8 +1935,9 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     const long long launches0 = s->prof.launches;
     s->matvecs = 0;
     s->inner_iters = 0;
+    s->active_mv = 0;
     s->graph_calls = 0;
-    CK(cudaMemsetAsync(s->d_iter, 0, 3 * sizeof(int), s->st));
+    CK(cudaMemsetAsync(s->d_iter, 0, 4 * sizeof(int), s->st));
     TRY(set_kappa_impl(s, kappa));
     TRY(autotune_plane(s, s->o.block));
     const long long N = 2 * s->nv;
@@ -1960,6 +1973,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
             stats->converged = conv ? 1 : 0;
             stats->inner_iters = 0;
             stats->matvecs = s->matvecs;
+            stats->active_matvecs = s->matvecs;   // LOBPCG applies A_r to the unlocked columns only
             stats->kernel_launches = s->prof.launches - launches0;
             stats->max_ritz_residual = maxres;
             stats->max_residual = maxres;
@@ -2182,6 +2196,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         for (int c0 = 0; c0 < want; c0 += b) {
             const int qc = std::min(b, want - c0);
             TRY(apply_op(s, Y + (size_t)c0 * N, AZ + (size_t)c0 * N, qc, BNF_OP_AR));
+            s->active_mv += qc;
         }
         std::vector<cd> Hm, Zs;
         TRY(gram_host(s, Y, want, AZ, want, Hm));
@@ -2226,10 +2241,11 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
     if (s->prof.on) s->prof.flush();
     long long graph_launches = 0;
     if (s->graph_calls > 0) {   // CG iterations run inside graphs were counted on the device
-        int h[3];
-        CK(cudaMemcpy(h, s->d_iter, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+        int h[4];
+        CK(cudaMemcpy(h, s->d_iter, 4 * sizeof(int), cudaMemcpyDeviceToHost));
         s->inner_iters += h[2];
         s->matvecs += h[2];
+        s->active_mv += h[3];
         graph_launches = (long long)h[1] * s->graph_kernels_per_iter;
     }
     if (stats) {
@@ -2241,6 +2257,7 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
         stats->max_ritz_residual = maxres;
         stats->max_residual = maxr_ar;
         stats->polish_steps = polish;
+        stats->active_matvecs = s->active_mv;
         stats->polish_failed = polish_failed;
         stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }

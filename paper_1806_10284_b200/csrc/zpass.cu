@@ -169,21 +169,15 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     __syncthreads();
     const ColS& c = cs[w];
     // ---- phase A: mode algebra, element e = (k, w), k = e / W ----
-#pragma unroll(RST == 2 ? J : 1)
-    for (int e = tid; e < TE; e += NT) {
+    // (RST 2: unrolled over jj with a compile-time trip count so that xb1 / xb2 stay in registers)
+    auto elem = [&](const int e, double2 x1, double2 x2) {
         const int k = e / W;
         double2 u1 = sm[e], u2 = sm[TE + e];
         if (MODE == 1) {
             const double2 q1 = sm[2 * TE + e], q2 = sm[3 * TE + e];
-            const double2 x1 = RST == 1 ? sm[4 * TE + e] : (RST == 2 ? xb1[(e - tid) / NT] : xn1);
-            const double2 x2 = RST == 1 ? sm[5 * TE + e] : (RST == 2 ? xb2[(e - tid) / NT] : xn2);
-            if (RST == 0) {
-                xn1 = xm1;
-                xn2 = xm2;
-                if (e + 2 * NT < TE) {
-                    xm1 = xcol[kstride * ((e + 2 * NT) / W)];
-                    xm2 = xcol[n + kstride * ((e + 2 * NT) / W)];
-                }
+            if (RST == 1) {
+                x1 = sm[4 * TE + e];
+                x2 = sm[5 * TE + e];
             }
             double2* xg = xcol + kstride * k;
             xg[0] = make_double2(fma(alpha_prev, q1.x, x1.x), fma(alpha_prev, q1.y, x1.y));   // x += alpha_prev p
@@ -202,6 +196,25 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         sm[e] = modes::comb(o, 0, U1, U2);           // component tiles alias the consumed inputs
         sm[TE + e] = modes::comb(o, 1, U1, U2);
         sm[2 * TE + e] = modes::comb(o, 2, U1, U2);
+    };
+    if (MODE == 1 && RST == 2) {
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj)
+            if (tid + jj * NT < TE) elem(tid + jj * NT, xb1[jj], xb2[jj]);
+    } else {
+#pragma unroll 1
+        for (int e = tid; e < TE; e += NT) {
+            const double2 x1 = xn1, x2 = xn2;
+            if (MODE == 1 && RST == 0) {   // x streamed two elements ahead
+                xn1 = xm1;
+                xn2 = xm2;
+                if (e + 2 * NT < TE) {
+                    xm1 = xcol[kstride * ((e + 2 * NT) / W)];
+                    xm2 = xcol[n + kstride * ((e + 2 * NT) / W)];
+                }
+            }
+            elem(e, x1, x2);
+        }
     }
     __syncthreads();
     // ---- phase B: z-DFT of component l over k, twiddle, store ----
@@ -312,8 +325,9 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     __syncthreads();
     // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
     double rr = 0.0;
-#pragma unroll(RST == 2 ? J : 1)
-    for (int e = tid; e < TE; e += NT) {
+    // RST 2: the element loop is unrolled over jj with a compile-time trip count so that rb1 / rb2
+    // stay in registers (indexing them by (e - tid) / NT put them on the stack)
+    auto elem = [&](const int e, double2 r1, double2 r2) {
         const int k = e / W;
         const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
         Coef o;
@@ -325,11 +339,9 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         z1 = cscale(z1, o.f1);
         z2 = cscale(z2, o.f2);
         if (MODE == 1) {
-            double2 r1 = RST == 1 ? sm[3 * TE + e] : (RST == 2 ? rb1[(e - tid) / NT] : rn1);
-            double2 r2 = RST == 1 ? sm[4 * TE + e] : (RST == 2 ? rb2[(e - tid) / NT] : rn2);
-            if (RST == 0 && e + NT < TE) {
-                rn1 = o1[kstride * ((e + NT) / W)];
-                rn2 = o1[n + kstride * ((e + NT) / W)];
+            if (RST == 1) {
+                r1 = sm[3 * TE + e];
+                r2 = sm[4 * TE + e];
             }
             r1 = make_double2(fma(-alpha, z1.x, r1.x), fma(-alpha, z1.y, r1.y));
             r2 = make_double2(fma(-alpha, z2.x, r2.x), fma(-alpha, z2.y, r2.y));
@@ -339,6 +351,21 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         } else {
             o1[kstride * k] = z1;
             o1[n + kstride * k] = z2;
+        }
+    };
+    if (MODE == 1 && RST == 2) {
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj)
+            if (tid + jj * NT < TE) elem(tid + jj * NT, rb1[jj], rb2[jj]);
+    } else {
+#pragma unroll 1
+        for (int e = tid; e < TE; e += NT) {
+            const double2 r1 = rn1, r2 = rn2;
+            if (MODE == 1 && RST == 0 && e + NT < TE) {   // next residual element in flight
+                rn1 = o1[kstride * ((e + NT) / W)];
+                rn2 = o1[n + kstride * ((e + NT) / W)];
+            }
+            elem(e, r1, r2);
         }
     }
     if (MODE == 1) {
@@ -396,7 +423,7 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
     const size_t smem = L::smem_fwd(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, double2* Pp, double2* Xp, CGFuse cgv) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(Y, U, a, opv, Pp, Xp, cgv);
         return cudaGetLastError();
@@ -418,7 +445,7 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
     const size_t smem = L::smem_adj(mode, rst);
     const dim3 g((unsigned)(a.mp.n1 / W), (unsigned)a.n2loc, (unsigned)nvec);
     auto go = [&](auto kern, int opv, CGFuse cgv) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
         kern<<<g, L::C::NT, smem, st>>>(U, OUT, a, opv, cgv);
         return cudaGetLastError();

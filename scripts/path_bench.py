@@ -76,6 +76,7 @@ def main():
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "failed_kpoints": failed,
                 "matvecs_per_kpoint": float(np.mean([r.stats.get("matvecs", 0) for r in recs])),
+                "active_matvecs_per_kpoint": float(np.mean([r.stats.get("active_matvecs", 0) for r in recs])),
                 "max_residual": max(r.stats.get("max_residual", float("nan")) for r in recs),
                 "residual_per_k": [float("%.3g" % r.stats.get("max_residual", float("nan"))) for r in recs],
                 "polish_steps_per_k": [int(r.stats.get("polish_steps", 0)) for r in recs],

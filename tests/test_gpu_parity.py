@@ -299,6 +299,10 @@ def test_graph_cg_equals_eager(bnf):
     assert np.array_equal(l1, l2)
     assert s1["matvecs"] == s2["matvecs"] and s1["inner_iters"] == s2["inner_iters"]
     assert s1["kernel_launches"] > 0 and s2["kernel_launches"] > 0
+    # applications to still-iterating right-hand sides: counted on the device inside the
+    # graph, on the host in the eager loop -- the same number, at most every application
+    assert s1["active_matvecs"] == s2["active_matvecs"]
+    assert 0 < s1["active_matvecs"] <= s1["matvecs"]
 
 
 def test_warm_start_same_eigenvalues(bnf):
@@ -554,6 +558,30 @@ def test_cg_fused_iterations_elementwise(bnf, monkeypatch, idx, kidx, middle):
             assert its == [k]
             err = np.abs(got[v] - want).max() / np.abs(want).max()
             assert err <= 1e-11, (middle, k, v, err)
+    S.close()
+
+
+@pytest.mark.parametrize("idx,kidx", [(3, 5), (4, 12)], ids=["96", "128"])
+@pytest.mark.parametrize("zcfg", [0, 1, 2, 4, 6, 8, 12])
+def test_cg_fused_zpass_variants(bnf, monkeypatch, idx, kidx, zcfg):
+    """Every z-pass tile / prefetch configuration (BNF_ZCFG bits: 1 staged
+    r and x tiles, 2 narrow tiles, 4 residual prefetch in registers, 8 x
+    prefetch in registers) gives the same CG iterates as plain CG on the
+    oracle's M, x_3 to 1e-11 relative, b = 2."""
+    cfg, n, kap = _cfg_case(idx, None, kidx)
+    L, O, eps, S = _forced_solver(bnf, monkeypatch, {"BNF_ZCFG": str(zcfg)}, cfg, n)
+    from oracle import eigsolve
+    op = fftop.NFSEPOperator(O, kap, eps)
+    S.set_kappa(kap)
+    c = vectors.complex_normal((2, 2 * O.nn), seed=11 + idx)
+    cd = torch.from_numpy(c).cuda()
+    xd = torch.empty_like(cd)
+    assert S.cg_solve(cd, xd, 2, 3) == 3
+    got = xd.cpu().numpy()
+    for v in range(2):
+        want, _ = eigsolve.cg(op.M, c[v], tol=0.0, maxit=3)
+        err = np.abs(got[v] - want).max() / np.abs(want).max()
+        assert err <= 1e-11, (zcfg, v, err)
     S.close()
 
 
