@@ -61,6 +61,8 @@ PASS_BYTES = {
     "plane_t_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     "plane_ts": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,     # TMA-staged, shuffle FFT exchange
     "plane_ts_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    "plane_tp": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,      # TMA-staged, shuffles, two planes per CTA
+    "plane_tp_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     # persistent pipelined z passes (zpass.cu); CG x update deferred into zfwd2_cg
     "zfwd2": lambda n: 2 * 16 * n + 3 * 16 * n,
     "zadj2": lambda n: 3 * 16 * n + 2 * 16 * n,
@@ -453,7 +455,7 @@ def main():
                    "converged": all(s_["converged"] for s_ in stats),
                    "max_residual": max(s_["max_residual"] for s_ in stats)},
         "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
-        "middle": ("plane_ts" if "plane_ts_cg" in ktimes else "plane_t" if "plane_t_cg" in ktimes else "plane_ws" if "plane_ws_cg" in ktimes else "plane_w" if "plane_w_cg" in ktimes
+        "middle": ("plane_tp" if "plane_tp_cg" in ktimes else "plane_ts" if "plane_ts_cg" in ktimes else "plane_t" if "plane_t_cg" in ktimes else "plane_ws" if "plane_ws_cg" in ktimes else "plane_w" if "plane_w_cg" in ktimes
                    else "plane_l2" if "plane_l2_cg" in ktimes else "plane_cluster" if "plane_cg" in ktimes
                    else "y/x/y"),
     }

@@ -144,7 +144,7 @@ __device__ __forceinline__ void fft_mirror_ip(double2 (&v)[N1], int t, int w, do
     fast::DFT<N1, S>::run(v);
 }
 
-template <int N1, int N2, int XS = 0>
+template <int N1, int N2, int XS = 0, int PR = 1>
 struct PlaneTCfg {
     static constexpr int N = N1 * N2;
     static constexpr int S = 16;                 // sequences per strip
@@ -152,30 +152,40 @@ struct PlaneTCfg {
     static constexpr int NT = S * N2;            // threads
     static constexpr int SE = S * N;             // complex elements per strip buffer
     static constexpr bool EPF = N <= 128 && !XS;  // whole-plane eps index prefetch (XS: 3 CTAs / SM instead)
-    // dynamic smem: 2 strip buffers (1024-aligned), roots, lut, eps, barriers
+    static constexpr bool EST = PR == 2;          // per-strip eps index prefetch (two strip buffers of S N bytes)
+    // dynamic smem: 2 strip buffers (1024-aligned), roots (y, x; PR 2: one table, n1 == n2), lut, eps, barriers
     static constexpr size_t off_root = (size_t)2 * SE * 16;
-    static constexpr size_t off_lut = off_root + (size_t)2 * N * 16;
+    static constexpr size_t off_lut = off_root + (size_t)(PR == 2 ? 1 : 2) * N * 16;
     static constexpr size_t off_eps = off_lut + 256 * 8;
-    static constexpr size_t off_bar = off_eps + (EPF ? (size_t)N * N : 0);
+    static constexpr size_t off_bar = off_eps + (EPF ? (size_t)N * N : EST ? (size_t)2 * S * N : 0);
     static constexpr size_t smem = off_bar + 64 + 1024;   // + alignment slack
 };
+template <int K>
+__device__ __forceinline__ void bulk_wait_k() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(K) : "memory"); }
 
 // XS = 0: sequence w = tid % 16 with its N2 threads in different warps, the FFT
 // stage exchange in place in the strip buffer (block barriers); XS = 1: the N2
 // threads of a sequence are consecutive lanes of one warp and the exchange is
 // an xor-shuffle transpose (fastfft warp_xpose): shared memory then only
 // carries the strip staging, and the strip needs no barrier until its store.
-template <int N1, int N2, int CG, int XS>
+// PR = 2 (XS = 1 only): each CTA transforms two planes c and c + n3 / 2 of one
+// component, phase by phase interleaved (y of A, y of B, x of A, x of B, y^-1 of
+// A, y^-1 of B), so that the first strip of a phase -- which reads what the
+// plane's previous phase stored -- is prefetched while the other plane's phase
+// runs instead of after a full store drain; the eps indices of the next x strip
+// are copied to shared memory one strip ahead (cp.async).
+template <int N1, int N2, int CG, int XS, int PR = 1>
 __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, XS>::NT <= 128 ? (XS ? 3 : 2) : 1)
     k_plane_t(OpArgs a, CGFuse cgf, const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap mx,
               int zbase) {
-    using C = PlaneTCfg<N1, N2, XS>;
+    using C = PlaneTCfg<N1, N2, XS, PR>;
     constexpr int N = C::N, S = C::S, P = C::P, NT = C::NT, SE = C::SE;
+    static_assert(PR == 1 || XS == 1, "paired planes: warp-shuffle exchange only");
     extern __shared__ unsigned char smraw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(smraw) + 1023) & ~(size_t)1023);
     double2* buf = reinterpret_cast<double2*>(sm);
     double2* ry = reinterpret_cast<double2*>(sm + C::off_root);
-    double2* rx = ry + N;
+    double2* rx = PR == 2 ? ry : ry + N;
     double* lut_s = reinterpret_cast<double*>(sm + C::off_lut);
     unsigned char* eps_s = sm + C::off_eps;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + C::off_bar);
@@ -183,11 +193,14 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
     const int tid = threadIdx.x;
     const int w = XS ? (tid / 32) * (32 / N2) + (tid % 32) / N2 : tid % S;
     const int t = XS ? tid % N2 : tid / S;
-    const int c = blockIdx.x;
+    const int c0 = blockIdx.x;
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
-    const int z = zbase + vl * p.n3 + c;          // plane index in the tensor maps
+    const int zb = zbase + vl * p.n3;               // plane index base in the tensor maps
+    const int cstep = p.n3 / PR;                     // PR 2: planes c0 and c0 + n3 / 2
     const bool epf = C::EPF && a.eps_idx != nullptr;
+    const bool est = C::EST && a.eps_idx != nullptr;
+    constexpr int G = 3 * P * PR;                    // strips per CTA
     if (tid == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
@@ -196,20 +209,22 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
     }
     for (int q = tid; q < N; q += NT) {
         ry[q] = __ldg(a.py.root2 + q);
-        rx[q] = __ldg(a.px.root2 + q);
+        if (PR == 1) rx[q] = __ldg(a.px.root2 + q);
     }
     if (a.eps_idx != nullptr)
         for (int q = tid; q < 256; q += NT) lut_s[q] = __ldg(a.eps_lut + q);
     if (epf) {
-        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c;
+        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * N * c0;
         for (int q = tid; q < N * N / 16; q += NT) cp_async16t(eps_s + 16 * q, src + 16 * q);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     __syncthreads();
-    // strip g (phase g / P, strip r = g % P) into buffer g % 2
+    // strip g: segment g / P = (phase, plane) = (seg / PR, seg % PR), strip r = g % P, buffer g % 2
+    auto plane_of = [&](int g) { return (g / P) % PR; };
+    auto phase_of = [&](int g) { return (g / P) / PR; };
     auto load = [&](int g) {
         double2* b = buf + (g & 1) * SE;
-        const int ph = g / P, r = g % P;
+        const int ph = phase_of(g), r = g % P, z = zb + c0 + cstep * plane_of(g);
         mbar_expect_tx(&full[g & 1], (unsigned)(SE * 16));
         if (ph != 1) {   // column strip: 2 boxes of 8 columns x N rows
 #pragma unroll
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
     };
     auto store = [&](int g) {
         const double2* b = buf + (g & 1) * SE;
-        const int ph = g / P, r = g % P;
+        const int ph = phase_of(g), r = g % P, z = zb + c0 + cstep * plane_of(g);
         if (ph != 1) {
 #pragma unroll
             for (int q = 0; q < S / 8; ++q) tma_store3(&my, (r * S + q * 8) * 2, 0, z, b + q * 8 * N);
@@ -231,6 +246,14 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
         }
         bulk_commit();
     };
+    // PR 2: eps indices of x strip g (S rows of N bytes) into eps buffer g % 2, every thread a share
+    auto eps_copy = [&](int g) {
+        const int r = g % P, cc = c0 + cstep * plane_of(g);
+        const unsigned char* src = a.eps_idx + (size_t)l * p.n + (size_t)N * ((size_t)r * S + (size_t)N * cc);
+        unsigned char* dst = eps_s + (g & 1) * (S * N);
+        for (int q = tid; q < S * N / 16; q += NT) cp_async16t(dst + 16 * q, src + 16 * q);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
     if (tid == 0) load(0);
     static_assert(!XS || 32 % N2 == 0, "warp-local exchange: N2 divides 32");
     const unsigned n12 = (unsigned)p.n12;
@@ -238,12 +261,27 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
     double pmp = 0.0;
     double2 v[N1];
 #pragma unroll 1
-    for (int g = 0; g < 3 * P; ++g) {
-        const int ph = g / P, r = g % P;
-        // prefetch the next strip of the same phase (its buffer's last store must have read smem)
-        if (tid == 0 && g + 1 < 3 * P && (g + 1) % P != 0) {
-            bulk_wait_read0();
-            load(g + 1);
+    for (int g = 0; g < G; ++g) {
+        const int ph = phase_of(g), r = g % P;
+        const int c = c0 + cstep * plane_of(g);
+        if (PR == 1) {
+            // prefetch the next strip of the same phase (its buffer's last store must have read smem)
+            if (tid == 0 && g + 1 < G && (g + 1) % P != 0) {
+                bulk_wait_read0();
+                load(g + 1);
+            }
+        } else if (g + 1 < G) {
+            if (tid == 0) {
+                bulk_wait_read0();   // buffer (g + 1) % 2: the store of strip g - 1 has read it
+                if ((g + 1) % P == 0 && phase_of(g + 1) > 0) {
+                    // first strip of a plane's next phase: that plane's previous phase was stored before
+                    // the P - 1 strips of the other plane committed since -- those may stay in flight
+                    bulk_wait_k<P - 1>();
+                    fence_async_global();
+                }
+                load(g + 1);
+            }
+            if (est && phase_of(g + 1) == 1) eps_copy(g + 1);
         }
         mbar_wait(&full[g & 1], (unsigned)((g >> 1) & 1));
         double2* b = buf + (g & 1) * SE;
@@ -287,7 +325,10 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
                         v[u * N2 + k2] = cscale(x, s_);
                     }
             };
-            if (epf) scale([&](int aa) { return lut_s[eps_s[brow * N + aa]]; });
+            if (est) {
+                const unsigned char* e = eps_s + (g & 1) * (S * N) + w * N;
+                scale([&](int aa) { return lut_s[e[aa]]; });
+            } else if (epf) scale([&](int aa) { return lut_s[eps_s[brow * N + aa]]; });
             else if (a.eps_idx) scale([&](int aa) { return lut_s[__ldg(a.eps_idx + rowofs + aa)]; });
             else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
             if constexpr (XS) fast::fft_mirror_w<N1, N2, -1, 1>(v, t, w, nullptr, rx);
@@ -313,11 +354,12 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
 #pragma unroll
                 for (int k2 = 0; k2 < N2; ++k2) b[LayY<N>::at(w, t + N2 * u + N1 * k2)] = v[u * N2 + k2];
         }
+        if (est) asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // next x strip's eps: in smem by the barrier
         fence_async_smem();   // generic-proxy writes of the strip -> visible to the TMA store
         __syncthreads();
         if (tid == 0) {
             store(g);
-            if (g + 1 < 3 * P && (g + 1) % P == 0) {
+            if (PR == 1 && g + 1 < G && (g + 1) % P == 0) {
                 // first strip of the next phase reads what this phase wrote: every store complete
                 bulk_wait0();
                 fence_async_global();
@@ -338,7 +380,8 @@ __global__ void __launch_bounds__(PlaneTCfg<N1, N2, XS>::NT, PlaneTCfg<N1, N2, X
 template <int N1, int N2>
 cudaError_t launch_plane_t_t(const OpArgs& a, int nslab, const CGFuse* cg, cudaStream_t st, const CUtensorMap& my,
                              const CUtensorMap& mx, int zbase) {
-    const dim3 g((unsigned)a.mp.n3, (unsigned)nslab);
+    const int pr = a.plane_t == 3 ? 2 : 1;
+    const dim3 g((unsigned)(a.mp.n3 / pr), (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg, size_t smem, int nt) -> cudaError_t {
         cudaError_t e = allow_smem((const void*)kern, smem);
         if (e != cudaSuccess) return e;
@@ -347,6 +390,11 @@ cudaError_t launch_plane_t_t(const OpArgs& a, int nslab, const CGFuse* cg, cudaS
     };
     using C0 = PlaneTCfg<N1, N2, 0>;
     using C1 = PlaneTCfg<N1, N2, 1>;
+    using C2 = PlaneTCfg<N1, N2, 1, 2>;
+    if (a.plane_t == 3) {
+        if (cg) return run(k_plane_t<N1, N2, 1, 1, 2>, *cg, C2::smem, C2::NT);
+        return run(k_plane_t<N1, N2, 0, 1, 2>, CGFuse{}, C2::smem, C2::NT);
+    }
     if (a.plane_t == 2) {
         if (cg) return run(k_plane_t<N1, N2, 1, 1>, *cg, C1::smem, C1::NT);
         return run(k_plane_t<N1, N2, 0, 1>, CGFuse{}, C1::smem, C1::NT);

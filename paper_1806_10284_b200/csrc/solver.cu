@@ -556,6 +556,7 @@ cudaError_t slab_exchange(bnf_solver* s, double2* U, double2* Ub, int nvec, int 
 }
 
 const char* plane_name(const OpArgs& a, bool cg) {
+    if (a.plane_t == 3) return cg ? "plane_tp_cg" : "plane_tp";
     if (a.plane_t) return a.plane_t == 2 ? (cg ? "plane_ts_cg" : "plane_ts") : (cg ? "plane_t_cg" : "plane_t");
     if (a.plane_w) return a.plane_w == 2 ? (cg ? "plane_ws_cg" : "plane_ws") : (cg ? "plane_w_cg" : "plane_w");
     if (a.plane_l2) return cg ? "plane_l2_cg" : "plane_l2";
@@ -656,6 +657,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
         s->args.plane_l2 = std::getenv("BNF_PLANE_L2") ? std::atoi(std::getenv("BNF_PLANE_L2")) : 0;
         s->args.plane_w = std::getenv("BNF_PLANE_W") ? std::atoi(std::getenv("BNF_PLANE_W")) : 0;
         s->args.plane_t = (std::getenv("BNF_PLANE_T") && s->plane_t_ok) ? std::max(1, std::atoi(std::getenv("BNF_PLANE_T"))) : 0;
+        if (s->args.plane_t == 3 && s->args.mp.n3 % 2 != 0) s->args.plane_t = 2;   // paired planes: n3 even
         if (std::getenv("BNF_NO_PLANE")) s->args.plane_w = s->args.plane_t = 0;
         s->use_plane = std::getenv("BNF_NO_PLANE") == nullptr;
         s->kver++;
@@ -672,10 +674,11 @@ int autotune_plane(bnf_solver* s, int nvec) {
     CK(cudaEventCreate(&e1));
     // variants: 0 = y / x / y passes, 1 = cluster plane (DSMEM), 2 = plane via L2,
     // 3 / 4 = plane via L2 with warp-local FFT exchanges (shared memory / shuffles),
-    // 5 / 6 = plane via L2 staged by TMA (exchange in shared memory / by warp shuffles)
-    const int nvar = s->plane_t_ok ? 7 : plane_w_supported(s->args) ? 5 : 3;
+    // 5 / 6 = plane via L2 staged by TMA (exchange in shared memory / by warp shuffles),
+    // 7 = TMA + shuffles, two planes per CTA phase-interleaved (n3 even)
+    const int nvar = s->plane_t_ok ? (s->args.mp.n3 % 2 == 0 ? 8 : 7) : plane_w_supported(s->args) ? 5 : 3;
     const int v0 = s->nsl > 1 ? 2 : 0;   // slab mode: plane passes through L2 only (slab-aware)
-    float best[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float best[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;

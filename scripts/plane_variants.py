@@ -22,7 +22,8 @@ from synthetic import configs  # noqa: E402
 
 VARIANTS = {"yxy": {"BNF_NO_PLANE": "1"}, "cluster": {"BNF_PLANE": "1"},
             "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"}, "warp_smem": {"BNF_PLANE_W": "1"},
-            "warp_shfl": {"BNF_PLANE_W": "2"}, "tma": {"BNF_PLANE_T": "1"}, "tma_shfl": {"BNF_PLANE_T": "2"}}
+            "warp_shfl": {"BNF_PLANE_W": "2"}, "tma": {"BNF_PLANE_T": "1"}, "tma_shfl": {"BNF_PLANE_T": "2"},
+            "tma_pair": {"BNF_PLANE_T": "3"}}
 
 
 def main():
