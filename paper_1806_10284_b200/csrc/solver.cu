@@ -1961,10 +1961,17 @@ int bnf_solve(bnf_solver* s, const double kappa[3], int nev, double* lambda, bnf
             // stagnation / breakdown: fall back to the paper's inverse Lanczos (cold start)
             s->lob_fallbacks++;
             s->prev_want = 0;
+            const long long lob_mv = s->matvecs, lob_launches = s->prof.launches - launches0;
             bnf_opts keep = s->o;
             s->o.method = 0;
             const int rc2 = bnf_solve(s, kappa, nev, lambda, stats);
             s->o = keep;
+            if (stats) {   // the abandoned LOBPCG iterations are part of this call's work
+                stats->matvecs += lob_mv;
+                stats->active_matvecs += lob_mv;
+                stats->kernel_launches += lob_launches;
+                stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            }
             return rc2;
         }
         s->nev_last = nev;
