@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--out", default=None)
     ap.add_argument("--warm", type=int, default=1)
-    ap.add_argument("--per-gpu", type=int, default=1, help="concurrent solvers (streams) per GPU")
+    ap.add_argument("--per-gpu", default="1", help="concurrent solvers (streams) per GPU, or auto")
     ap.add_argument("--relax-inner", type=int, default=0)
     ap.add_argument("--method", type=int, default=0, help="0 inverse Lanczos (paper), 1 LOBPCG (NEXT-1)")
     ap.add_argument("--kmax", type=int, default=0, help="only the first kmax k-points of each path")
@@ -57,7 +57,8 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         extra = {"guard": a.guard} if a.guard is not None else {}
-        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=a.per_gpu,
+        pg = kpath.auto_per_gpu(cfg.n) if a.per_gpu == "auto" else int(a.per_gpu)
+        recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=pg,
                                 relax_inner=a.relax_inner, method=a.method, **extra)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
@@ -72,7 +73,7 @@ def main():
                 g = np.asarray(gold[key][:len(r.lam)])
                 dev.append(float(np.max(np.abs(np.asarray(r.lam[:len(g)]) - g) / g)))
         line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
-                "per_gpu": a.per_gpu, "relax_inner": a.relax_inner, "method": a.method,
+                "per_gpu": pg, "relax_inner": a.relax_inner, "method": a.method,
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "failed_kpoints": failed,
                 "matvecs_per_kpoint": float(np.mean([r.stats.get("matvecs", 0) for r in recs])),

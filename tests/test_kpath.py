@@ -202,3 +202,8 @@ def test_band_gaps():
     g = kpath.band_gaps(recs)
     assert len(g) == 1 and g[0][0] == 1
     assert abs(g[0][1] - 0.3) < 1e-12 and abs(g[0][2] - 0.4) < 1e-12 and abs(g[0][3] - 0.1) < 1e-12
+
+
+def test_auto_per_gpu():
+    assert kpath.auto_per_gpu((12, 12, 12)) == 3 and kpath.auto_per_gpu((64, 64, 64)) == 3
+    assert kpath.auto_per_gpu((96, 96, 96)) == 2 and kpath.auto_per_gpu((128, 128, 128)) == 1
