@@ -68,6 +68,9 @@ PASS_BYTES = {
     "zadj2": lambda n: 3 * 16 * n + 2 * 16 * n,
     "zfwd2_cg": lambda n: 6 * 16 * n + 4 * 16 * n + 3 * 16 * n,   # read r,p,x; write p,x; write U
     "zadj2_cg": lambda n: 3 * 16 * n + 4 * 16 * n,                 # read U, r; write r
+    # persistent TMA-pipelined adjoint z pass (zpipe.cu): same bytes as zadj2
+    "zadj3": lambda n: 3 * 16 * n + 2 * 16 * n,
+    "zadj3_cg": lambda n: 3 * 16 * n + 4 * 16 * n,
 }
 
 
@@ -241,8 +244,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours")
-    ap.add_argument("--block", type=int, default=2)
+    # defaults from profiles/r03_bench_block_sweep.jsonl (128^3, k12-k15): block 1 needs 22 % fewer
+    # operator applications per k-point than block 2 (2766 vs 3570) at 5 % lower matvec rate; two
+    # concurrent solvers per GPU recover most of that rate (the b = 1 launches underfill the GPU)
+    ap.add_argument("--block", type=int, default=1)
     ap.add_argument("--guard", type=int, default=2)
+    ap.add_argument("--per-gpu", type=int, default=2,
+                    help="concurrent solvers (one stream + host thread each) per GPU; a step solves one k-point each")
     ap.add_argument("--warm", type=int, default=1,
                     help="start each k-point from the previous one's Ritz vectors (DESIGN R17)")
     ap.add_argument("--kstart", type=int, default=12, help="path index of the first timed k-point")
@@ -282,54 +290,90 @@ def main():
     lat = bnf.Lattice(cfg.a_raw, cfg.n)
     eps = eps_for(cfg, lat)
     ks = kappas(cfg, lat)
-    stream = torch.cuda.Stream()
-    S = bnf.Solver(lat, device=local, stream=stream.cuda_stream, profile=0, block=args.block, guard=args.guard,
-                   warm=args.warm, relax_inner=args.relax_inner)
-    S.set_epsilon(eps)
+    C = max(1, args.per_gpu)
+    streams = [torch.cuda.Stream() for _ in range(C)]
+    solvers = []
+    for c in range(C):
+        Sc = bnf.Solver(lat, device=local, stream=streams[c].cuda_stream, profile=0, block=args.block,
+                        guard=args.guard, warm=args.warm, relax_inner=args.relax_inner)
+        Sc.set_epsilon(eps)
+        solvers.append(Sc)
+    S, stream = solvers[0], streams[0]
     nev = cfg.nev
 
     share = kpath.assign(ks, world)[rank]   # LPT share of the path (no data-path collective)
 
     # the timed steps start at path point --kstart (k12 by default: the middle of the path, whose oracle
-    # golden exists; with --steps 12 or more the timed k-points also cover k23 and k0 = Gamma)
+    # golden exists; with --steps 12 or more the timed k-points also cover k23 and k0 = Gamma).  With C
+    # solvers per GPU, solver c walks its own contiguous run of the share (warm starts stay adjacent):
+    # its timed k-points start C * steps positions after solver c - 1's.
     off = (share.index(args.kstart) - args.warmup) % len(share) if args.kstart in share else 0
 
-    def kidx(step):
-        return share[(step + off) % len(share)]
+    def kidx(step, c=0):
+        return share[(step + c * args.steps + off) % len(share)]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def run_all(fn):
+        """fn(c) on every solver, concurrently (one host thread each; the C ABI releases the GIL)."""
+        if C == 1:
+            return [fn(0)]
+        out = [None] * C
+        err = []
+
+        def th(c):
+            try:
+                out[c] = fn(c)
+            except BaseException as e:   # re-raised below
+                err.append(e)
+        ths = [threading.Thread(target=th, args=(c,)) for c in range(C)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        if err:
+            raise err[0]
+        return out
+
     # warm-up (untimed)
-    for s in range(args.warmup):
-        S.solve(ks[kidx(s)], nev, allow_noconv=True)
-    S.kernel_times(reset=True)
+    run_all(lambda c: [solvers[c].solve(ks[kidx(s_, c)], nev, allow_noconv=True) for s_ in range(args.warmup)])
+    for Sc in solvers:
+        Sc.kernel_times(reset=True)
     # timed: device-resident inputs
     barrier()
     torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    mv = 0
-    launches = 0
-    stats = []
-    lams = []
+
+    def timed(c):
+        res = []
+        for s_ in range(args.steps):
+            k = kidx(args.warmup + s_, c)
+            lam, st = solvers[c].solve(ks[k], nev, allow_noconv=True)
+            res.append((k, lam, st))
+        return res
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for s in range(args.steps):
-            lam, st = S.solve(ks[kidx(args.warmup + s)], nev, allow_noconv=True)
-            mv += st["matvecs"]
-            launches += st["kernel_launches"]
-            stats.append(st)
-            lams.append((kidx(args.warmup + s), lam))
-        ev1.record(stream)
+        ev0.record(main)
+        for st_ in streams:
+            st_.wait_event(ev0)
+        per = run_all(timed)
+        for st_ in streams:
+            main.wait_stream(st_)
+        ev1.record(main)
         torch.cuda.synchronize()
     barrier()
     ms = ev0.elapsed_time(ev1)
-    # Kernel profile (roofline): one more k-point of this rank's share, run with
-    # per-kernel CUDA events on the solver's stream.  The timed steps above run
-    # the CG loop as a CUDA graph (no per-iteration host round trip); this pass
-    # launches the same kernels eagerly so each one can be bracketed by events.
+    mv = sum(st["matvecs"] for r in per for _, _, st in r)
+    launches = sum(st["kernel_launches"] for r in per for _, _, st in r)
+    stats = [st for r in per for _, _, st in r]
+    lams = [(k, lam) for r in per for k, lam, _ in r]
+    # Kernel profile (roofline): one more k-point of this rank's share, run by solver 0 alone with
+    # per-kernel CUDA events on its stream.  The timed steps above run the CG loop as a CUDA graph
+    # (no per-iteration host round trip); this pass launches the same kernels eagerly so each one can
+    # be bracketed by events.
     S.set_profile(1)
     S.kernel_times(reset=True)
     evp0 = torch.cuda.Event(enable_timing=True)
@@ -353,7 +397,7 @@ def main():
     else:
         ms_max, mv_tot = ms, float(mv)
     value = mv_tot / (ms_max / 1000.0)
-    kps = world * args.steps / (ms_max / 1000.0)
+    kps = world * C * args.steps / (ms_max / 1000.0)
 
     # e2e: host buffers through the C ABI (eps H2D + lambda D2H inside the timed region)
     e2e = None
@@ -361,11 +405,15 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        mv2 = 0
-        for s in range(args.steps):
-            S.set_epsilon(eps)                  # host -> device every step
-            lam, st = S.solve(ks[kidx(args.warmup + s)], nev, allow_noconv=True)   # lambda -> host
-            mv2 += st["matvecs"]
+
+        def e2e_run(c):
+            m = 0
+            for s_ in range(args.steps):
+                solvers[c].set_epsilon(eps)      # host -> device every step
+                lam, st = solvers[c].solve(ks[kidx(args.warmup + s_, c)], nev, allow_noconv=True)   # lambda -> host
+                m += st["matvecs"]
+            return m
+        mv2 = sum(run_all(e2e_run))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         t2 = torch.tensor([dt, mv2], dtype=torch.float64, device="cuda")
@@ -375,8 +423,8 @@ def main():
             s2 = t2.clone()
             dist.all_reduce(s2, op=dist.ReduceOp.SUM)
             dt, mv2 = float(m2[0]), float(s2[1])
-        e2e = {"value": mv2 / dt, "unit": "matvecs/s", "h2d_bytes_per_step": int(eps.nbytes),
-               "d2h_bytes_per_step": int(8 * nev), "kpoints_per_s": world * args.steps / dt}
+        e2e = {"value": mv2 / dt, "unit": "matvecs/s", "h2d_bytes_per_step": int(eps.nbytes) * C,
+               "d2h_bytes_per_step": int(8 * nev * C), "kpoints_per_s": world * C * args.steps / dt}
 
     if rank != 0:
         if world > 1:
@@ -433,13 +481,15 @@ def main():
               "max_rel_dev_vs_oracle": max(devs) if devs else None}
     line = {
         "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "kpoints_per_step": C, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "grid": list(cfg.n), "nev": nev, "kpoints_on_path": len(ks),
                    "block": args.block, "guard": args.guard, "tol_outer": 1e-12, "tol_inner": 1e-13,
                    "warm_start": bool(args.warm), "relax_inner": bool(args.relax_inner),
                    "l2": "inputs larger than L2 (Krylov basis and work arrays >> 126 MB)",
-                   "parallelism": "k-point replicas x%d" % world},
+                   "solvers_per_gpu": C,
+                   "parallelism": "k-point replicas x%d (x%d concurrent solvers per GPU)" % (world, C)},
         "kpoints_per_s": kps,
         "matvec_pipeline": {"ms_total": matvec_ms, "algorithmic_GBps": matvec_bytes / (matvec_ms / 1e3) / 1e9
                             if matvec_ms else None, "share_of_step": matvec_ms / ms_prof,
@@ -450,7 +500,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "solver": {"matvecs_per_kpoint": mv / args.steps,
+        "solver": {"matvecs_per_kpoint": mv / (C * args.steps),
                    "outer_steps": [s_["outer_steps"] for s_ in stats],
                    "converged": all(s_["converged"] for s_ in stats),
                    "max_residual": max(s_["max_residual"] for s_ in stats)},

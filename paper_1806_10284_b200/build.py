@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["kernels.cu", "plane.cu", "plane_tma.cu", "zpass.cu", "solver.cu", "lattice.cpp", "linalg_host.cpp"]
+SOURCES = ["kernels.cu", "plane.cu", "plane_tma.cu", "zpass.cu", "zpipe.cu", "solver.cu", "lattice.cpp", "linalg_host.cpp"]
 
 
 def _deps():

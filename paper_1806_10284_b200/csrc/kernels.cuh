@@ -131,6 +131,12 @@ bool plane_w_supported(const OpArgs& a);
 // TMA-staged plane pass (plane_tma.cu): one slab, square 64/128/256 planes.  The
 // tensor maps describe the plane buffer as [planes][N][2N doubles] (plane_t_encode).
 bool plane_t_supported(const OpArgs& a);
+// persistent TMA-pipelined adjoint z pass (zpipe.cu); the map views U as [comp slabs][n3][n2][2 n1 doubles]
+bool zadj3_supported(const OpArgs& a);
+int zadj3_tiles_x(const OpArgs& a);
+int zadj3_encode(const OpArgs& a, void* base, long long comp_slabs, void* encode_fn, CUtensorMap* m);
+cudaError_t launch_zadj3(const OpArgs& a, const CUtensorMap& tm, const double2* U, double2* OUT, int nvec, int op,
+                         const CGFuse* cg, cudaStream_t st);
 int plane_t_encode(const OpArgs& a, void* base, long long planes, void* encode_fn, CUtensorMap* my, CUtensorMap* mx);
 cudaError_t launch_plane_tma(const OpArgs& a, int nslab, const CGFuse* cg, cudaStream_t st, const CUtensorMap& my,
                              const CUtensorMap& mx, int zbase);

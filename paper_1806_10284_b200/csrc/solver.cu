@@ -404,6 +404,10 @@ struct bnf_solver {
     alignas(64) CUtensorMap tm_y, tm_x;   // TMA maps of U (plane_tma.cu), valid for (tm_base, tm_planes)
     void* tm_base = nullptr;
     long long tm_planes = 0;
+    bool use_z3 = false;      // persistent TMA-pipelined adjoint z pass (zpipe.cu)
+    alignas(64) CUtensorMap tm_zu;        // TMA map of U for k_zadj3, valid for (tm_zu_base, tm_zu_slabs)
+    void* tm_zu_base = nullptr;
+    long long tm_zu_slabs = 0;
     DevBuf Ub;                // plane-side buffer of the slab exchange (3n per vector)
     Profiler prof;
     long long matvecs = 0;
@@ -592,6 +596,24 @@ cudaError_t run_plane(bnf_solver* s, const OpArgs& a, double2* U, int nslab, con
     return launch_plane(a, U, nslab, cg, st);
 }
 
+// the adjoint z pass on U (one slab): the TMA-pipelined k_zadj3 when enabled, else k_zadj2
+cudaError_t run_zadj(bnf_solver* s, double2* U, double2* out, int nvec, int op, const CGFuse* cg, cudaStream_t st) {
+    if (s->use_z3) {
+        const long long slabs = (long long)(s->U.bytes / sizeof(double2)) / s->n;
+        if (s->tm_zu_base != s->U.p || s->tm_zu_slabs != slabs) {
+            if (zadj3_encode(s->args, s->U.p, slabs, tensor_map_encoder(), &s->tm_zu) != 0) return cudaErrorInvalidValue;
+            s->tm_zu_base = s->U.p;
+            s->tm_zu_slabs = slabs;
+        }
+        if (U != s->U.as<double2>()) return cudaErrorInvalidValue;
+        return launch_zadj3(s->args, s->tm_zu, U, out, nvec, op, cg, st);
+    }
+    return launch_zadj2(s->args, U, out, nvec, op, cg, st);
+}
+const char* zadj_name(const bnf_solver* s, bool cg) {
+    return s->use_z3 ? (cg ? "zadj3_cg" : "zadj3") : (cg ? "zadj2_cg" : "zadj2");
+}
+
 // out = op(y) for nvec vectors (device pointers, 2n each)
 int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
     TRY(ensure_work(s, nvec));
@@ -632,7 +654,7 @@ int apply_op(bnf_solver* s, const double2* y, double2* out, int nvec, int op) {
         RUN("xpass", launch_xpass(s->args, U, nvec, s->st));
         RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
     }
-    if (s->use_z2) RUN("zadj2", launch_zadj2(s->args, U, out, nvec, op, nullptr, s->st));
+    if (s->use_z2) RUN(zadj_name(s, false), run_zadj(s, U, out, nvec, op, nullptr, s->st));
     else RUN("zadj", launch_zadj(s->args, U, out, nvec, op, s->st));
     s->matvecs += nvec;
     return BNF_OK;
@@ -837,7 +859,7 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
         BNF_K(launch_cg_finish(cg, 0, nvec, st));
         BNF_K(launch_ypass(s->args, U, nvec, 1, st));
     }
-    if (s->use_z2) BNF_K(launch_zadj2(s->args, U, R, nvec, 1, &cg, st));
+    if (s->use_z2) BNF_K(run_zadj(s, U, R, nvec, 1, &cg, st));
     else BNF_K(launch_zadj_cg(s->args, U, X, nvec, cg, st));
     BNF_K(launch_cg_finish(cg, 1, nvec, st));
 #undef BNF_K
@@ -964,7 +986,7 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
                 RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
                 RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
             }
-            if (s->use_z2) RUN("zadj2_cg", launch_zadj2(s->args, U, R, nvec, 1, &cg, s->st));
+            if (s->use_z2) RUN(zadj_name(s, true), run_zadj(s, U, R, nvec, 1, &cg, s->st));
             else RUN("zadj_cg", launch_zadj_cg(s->args, U, X, nvec, cg, s->st));
             RUN("cg_beta", launch_cg_finish(cg, 1, nvec, s->st));
             }
@@ -1675,6 +1697,11 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->use_graph = std::getenv("BNF_NO_GRAPH") == nullptr;
     s->plane_t_ok = s->use_z2 && plane_t_supported(s->args) && tensor_map_encoder() != nullptr &&
                     std::getenv("BNF_NO_PLANE_T") == nullptr;
+    // persistent pipelined adjoint z pass (same tile width as k_zadj2, so the CG partial
+    // layout is unchanged): opt-in with BNF_Z3=1 -- measured slower than k_zadj2 (128^3, b = 2: 161 vs
+    // 133 us), so k_zadj2 stays the default
+    s->use_z3 = s->use_z2 && zadj3_supported(s->args) && !(s->args.zcfg & 2) && tensor_map_encoder() != nullptr &&
+                std::getenv("BNF_Z3") != nullptr && std::atoi(std::getenv("BNF_Z3")) != 0 && o.slabs <= 1;
     // virtual slabs (SURVEY §8(e) / DESIGN §8): the slab-decomposed operator with the
     // all-to-alls as device copies; needs the fast z passes and an L2 plane middle
     s->nsl = std::max(1, o.slabs);

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--method", type=int, default=0, help="0 inverse Lanczos (paper), 1 LOBPCG (NEXT-1)")
     ap.add_argument("--kmax", type=int, default=0, help="only the first kmax k-points of each path")
     ap.add_argument("--guard", type=int, default=None)
+    ap.add_argument("--block", type=int, default=None)
     a = ap.parse_args()
     gold = goldens()
     res = []
@@ -57,6 +58,8 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         extra = {"guard": a.guard} if a.guard is not None else {}
+        if a.block is not None:
+            extra["block"] = a.block
         pg = kpath.auto_per_gpu(cfg.n) if a.per_gpu == "auto" else int(a.per_gpu)
         recs = kpath.solve_path(cfg.a_raw, cfg.n, eps, ks, cfg.nev, device=0, warm=a.warm, per_gpu=pg,
                                 relax_inner=a.relax_inner, method=a.method, **extra)
@@ -73,7 +76,7 @@ def main():
                 g = np.asarray(gold[key][:len(r.lam)])
                 dev.append(float(np.max(np.abs(np.asarray(r.lam[:len(g)]) - g) / g)))
         line = {"config": cfg.name, "grid": list(cfg.n), "nev": cfg.nev, "kpoints": len(ks), "seconds": round(dt, 3),
-                "per_gpu": pg, "relax_inner": a.relax_inner, "method": a.method,
+                "per_gpu": pg, "block": extra.get("block"), "guard": extra.get("guard"), "relax_inner": a.relax_inner, "method": a.method,
                 "kpoints_per_s": len(ks) / dt, "status": sorted({r.status for r in recs}),
                 "failed_kpoints": failed,
                 "matvecs_per_kpoint": float(np.mean([r.stats.get("matvecs", 0) for r in recs])),

@@ -793,3 +793,36 @@ def test_gyroid_bcc_vs_dense_oracle(bnf):
     dense = np.linalg.eigvalsh(spectral.Ar_dense(O, kap, eps))[:8]
     lam, _ = S.solve(kap, 8)
     np.testing.assert_allclose(lam, dense, rtol=1e-10)
+
+
+@pytest.mark.parametrize("idx,kidx", [(4, 12)], ids=["128"])
+@pytest.mark.parametrize("zcfg", [4, 36, 68])
+def test_zadj3_equals_zadj2(bnf, monkeypatch, idx, kidx, zcfg):
+    """The persistent pipelined adjoint z pass (zpipe.cu; opt-in
+    BNF_Z3=1) does k_zadj2's arithmetic in the same order, partials included:
+    A_r applies and 3 fused CG iterations (b = 2, the bench's launch) are
+    bit-identical with k_zadj2, for the 3- and 2-buffer rings (cp.async) and
+    the TMA-copy ring; the CG iterates also equal plain CG on the oracle's M
+     to 1e-11."""
+    from oracle import eigsolve
+    cfg, n, kap = _cfg_case(idx, None, kidx)
+    res = {}
+    for name, envs in (("z3", {"BNF_ZCFG": str(zcfg), "BNF_Z3": "1"}), ("z2", {"BNF_ZCFG": str(zcfg)})):
+        L, O, eps, S = _forced_solver(bnf, monkeypatch, envs, cfg, n)
+        S.set_kappa(kap)
+        c = vectors.complex_normal((2, 2 * O.nn), seed=5 + idx)
+        cd = torch.from_numpy(c).cuda()
+        xd = torch.empty_like(cd)
+        assert S.cg_solve(cd, xd, 2, 3) == 3
+        od = torch.empty_like(cd)
+        S.apply_Ar(cd, od, 2, bnf.OP_AR)
+        torch.cuda.synchronize()
+        res[name] = (xd.cpu().numpy(), od.cpu().numpy())
+        S.close()
+    assert np.array_equal(res["z3"][0], res["z2"][0])
+    assert np.array_equal(res["z3"][1], res["z2"][1])
+    if idx == 4:
+        op = fftop.NFSEPOperator(O, kap, eps)
+        want, _ = eigsolve.cg(op.M, c[0], tol=0.0, maxit=3)
+        err = np.abs(res["z3"][0][0] - want).max() / np.abs(want).max()
+        assert err <= 1e-11, err
