@@ -52,6 +52,8 @@ PASS_BYTES = {
     "plane_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     "plane_l2": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,     # same bytes, strips exchanged through L2
     "plane_l2_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
+    "plane_l2s": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,    # L2 plane on a 2-CTA cluster per plane
+    "plane_l2s_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     # warp-local FFT exchange variants of the L2 plane pass (smem / shuffles): same bytes
     "plane_w": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
     "plane_w_cg": lambda n: 2 * 3 * 16 * n + 3 * 1 * n,
@@ -505,7 +507,7 @@ def main():
                    "converged": all(s_["converged"] for s_ in stats),
                    "max_residual": max(s_["max_residual"] for s_ in stats)},
         "kernel_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
-        "middle": ("plane_tp" if "plane_tp_cg" in ktimes else "plane_ts" if "plane_ts_cg" in ktimes else "plane_t" if "plane_t_cg" in ktimes else "plane_ws" if "plane_ws_cg" in ktimes else "plane_w" if "plane_w_cg" in ktimes
+        "middle": ("plane_l2s" if "plane_l2s_cg" in ktimes else "plane_tp" if "plane_tp_cg" in ktimes else "plane_ts" if "plane_ts_cg" in ktimes else "plane_t" if "plane_t_cg" in ktimes else "plane_ws" if "plane_ws_cg" in ktimes else "plane_w" if "plane_w_cg" in ktimes
                    else "plane_l2" if "plane_l2_cg" in ktimes else "plane_cluster" if "plane_cg" in ktimes
                    else "y/x/y"),
     }

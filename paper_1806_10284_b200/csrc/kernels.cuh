@@ -71,6 +71,7 @@ struct OpArgs {
                                 // tiles, bit 2 = CG residual of zadj prefetched into registers before the mode loop
                                 // (default on), bit 3 = CG x of zfwd prefetched into registers (measured slower)
     int plane_t;                // plane pass staged by TMA (plane_tma.cu)
+    int plane_split;            // L2 plane pass: 2 = a cluster of two CTAs per plane (every other strip each)
 };
 
 struct Profiler;  // host-side, see solver.cu

@@ -277,14 +277,19 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 // memory: the plane (N*N*16 B, 256 KB at 128^2) is re-read while it is hot
 // in L2, so DRAM still sees one read and one write per element, and there
 // are no cluster barriers or DSMEM stores.  Two CTAs per SM overlap.
-template <int N1, int N2, int P, int CG, int SL = 0>
+// SPLIT = 2: a cluster of two CTAs per plane, each taking every other strip of
+// every phase (the phases meet at a cluster barrier, whose release / acquire
+// orders the strips written through L2): twice the CTAs, half the work each,
+// so the last wave of the launch is half as long.
+template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1>
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
     extern __shared__ double2 D[];
     const ModeP& p = a.mp;
     const int tid = threadIdx.x;
-    const int c = blockIdx.x;
+    const int c = blockIdx.x / SPLIT;
+    const int r0 = SPLIT == 1 ? 0 : (int)(blockIdx.x % SPLIT);
     const int vl = blockIdx.y + a.comp0;
     const int l = vl % 3;
     // plane rows b: one slab -> plane + b N; virtual / distributed slabs -> the block of the
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     const unsigned long long pol_keep = a.plane_hint ? l2_policy_last() : 0ull;
     const unsigned long long pol_out = a.plane_hint ? l2_policy_first() : 0ull;
     // ---------------- phase Y: column strips ----------------
-    for (int r = 0; r < P; ++r) {
+    for (int r = r0; r < P; r += SPLIT) {
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
@@ -335,10 +340,11 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         }
     }
     if (epf) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();   // the strips written above are read by other threads below (block scope)
+    if constexpr (SPLIT == 1) __syncthreads();   // the strips written above are read by other threads below
+    else Cluster<2>::sync();                     // ... and by the other CTA of the plane (cluster release / acquire)
     // ---------------- phase X: row strips ----------------
     double pmp = 0.0;
-    for (int r = 0; r < P; ++r) {
+    for (int r = r0; r < P; r += SPLIT) {
         const int b = r * CW + rw;
         double2* row = rowp(b);
 #pragma unroll
@@ -370,9 +376,10 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             for (int m = 0; m < N1; ++m) row[N2 * m + tx] = v[m];
         }
     }
-    __syncthreads();
+    if constexpr (SPLIT == 1) __syncthreads();
+    else Cluster<2>::sync();
     // ---------------- phase Y*: column strips ----------------
-    for (int r = 0; r < P; ++r) {
+    for (int r = r0; r < P; r += SPLIT) {
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
@@ -581,6 +588,27 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
     if (a.nslab > 1) {
         if (cg) return run(k_plane_l2<N1, N2, P, 1, 1>, *cg);
         return run(k_plane_l2<N1, N2, P, 0, 1>, CGFuse{});
+    }
+    if (a.plane_split == 2 && P % 2 == 0) {   // cluster of two CTAs per plane
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * a.n3loc), (unsigned)nslab);
+        cfg.blockDim = dim3(C::NT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        auto run2 = [&](auto kern, auto cgarg) -> cudaError_t {
+            cudaError_t e = allow_smem((const void*)kern, smem);
+            if (e != cudaSuccess) return e;
+            return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg);
+        };
+        if (cg) return run2(k_plane_l2<N1, N2, P, 1, 0, 2>, *cg);
+        return run2(k_plane_l2<N1, N2, P, 0, 0, 2>, CGFuse{});
     }
     if (cg) return run(k_plane_l2<N1, N2, P, 1>, *cg);
     return run(k_plane_l2<N1, N2, P, 0>, CGFuse{});

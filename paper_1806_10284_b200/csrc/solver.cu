@@ -563,6 +563,7 @@ const char* plane_name(const OpArgs& a, bool cg) {
     if (a.plane_t == 3) return cg ? "plane_tp_cg" : "plane_tp";
     if (a.plane_t) return a.plane_t == 2 ? (cg ? "plane_ts_cg" : "plane_ts") : (cg ? "plane_t_cg" : "plane_t");
     if (a.plane_w) return a.plane_w == 2 ? (cg ? "plane_ws_cg" : "plane_ws") : (cg ? "plane_w_cg" : "plane_w");
+    if (a.plane_l2 && a.plane_split == 2) return cg ? "plane_l2s_cg" : "plane_l2s";
     if (a.plane_l2) return cg ? "plane_l2_cg" : "plane_l2";
     return cg ? "plane_cg" : "plane";
 }
@@ -700,17 +701,21 @@ int autotune_plane(bnf_solver* s, int nvec) {
     // 7 = TMA + shuffles, two planes per CTA phase-interleaved (n3 even)
     const int nvar = s->plane_t_ok ? (s->args.mp.n3 % 2 == 0 ? 8 : 7) : plane_w_supported(s->args) ? 5 : 3;
     const int v0 = s->nsl > 1 ? 2 : 0;   // slab mode: plane passes through L2 only (slab-aware)
-    float best[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float best[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool prof = s->prof.on;
     s->prof.on = false;
     const long long mv0 = s->matvecs;
+    // 8 = plane via L2 on a cluster of two CTAs per plane (every other strip each; one slab)
     auto set = [&](int variant) {
         s->use_plane = variant >= 1;
-        s->args.plane_l2 = variant == 2 ? 1 : 0;
+        s->args.plane_l2 = (variant == 2 || variant == 8) ? 1 : 0;
+        s->args.plane_split = variant == 8 ? 2 : 1;
         s->args.plane_w = (variant == 3 || variant == 4) ? variant - 2 : 0;
-        s->args.plane_t = variant >= 5 ? variant - 4 : 0;
+        s->args.plane_t = (variant >= 5 && variant <= 7) ? variant - 4 : 0;
     };
-    for (int variant = v0; variant < nvar; ++variant) {
+    const int nvar_all = s->nsl == 1 ? 9 : nvar;
+    for (int variant = v0; variant < nvar_all; ++variant) {
+        if (variant >= nvar && variant != 8) continue;
         if (s->nsl > 1 && variant >= 5) continue;   // TMA plane: one slab only
         set(variant);
         TRY(apply_op(s, y.as<double2>(), o.as<double2>(), nvec, BNF_OP_M));   // warm-up
@@ -721,7 +726,7 @@ int autotune_plane(bnf_solver* s, int nvec) {
         CK(cudaEventElapsedTime(&best[variant], e0, e1));
     }
     int pick = v0;
-    for (int variant = v0 + 1; variant < nvar; ++variant)
+    for (int variant = v0 + 1; variant < nvar_all; ++variant)
         if (best[variant] > 0.f && best[variant] < best[pick]) pick = variant;
     set(pick);
     s->matvecs = mv0;
@@ -1715,6 +1720,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
         }
     }
     s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
+    s->args.plane_split = std::getenv("BNF_PLANE_SPLIT") ? std::atoi(std::getenv("BNF_PLANE_SPLIT")) : 1;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

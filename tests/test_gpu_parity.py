@@ -494,11 +494,12 @@ def test_block_sizes_cg_solve(bnf, block):
 
 MIDDLES = {"cluster": {"BNF_PLANE": "1"}, "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"},
            "yxy": {"BNF_NO_PLANE": "1"}, "warp_smem": {"BNF_PLANE_W": "1"}, "warp_shfl": {"BNF_PLANE_W": "2"},
-           "tma": {"BNF_PLANE_T": "1"}, "tma_shfl": {"BNF_PLANE_T": "2"}, "tma_pair": {"BNF_PLANE_T": "3"}}
+           "tma": {"BNF_PLANE_T": "1"}, "tma_shfl": {"BNF_PLANE_T": "2"}, "tma_pair": {"BNF_PLANE_T": "3"},
+           "l2_split": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_SPLIT": "2"}}
 
 
 def _forced_solver(bnf, monkeypatch, envs, cfg, n, **kw):
-    for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T"):
+    for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T", "BNF_PLANE_SPLIT"):
         monkeypatch.delenv(k, raising=False)
     for k, v in envs.items():
         monkeypatch.setenv(k, v)
