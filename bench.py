@@ -459,7 +459,11 @@ def main():
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get(name)
+                tj = json.load(f)
+            if tj.get(name) is not None:
+                # DRAM bytes per launch from the ncu capture, scaled to this launch's vector count
+                vcap = float(tj.get("_vectors_per_launch", 2))
+                traffic = tj[name] * (total_bytes / kcnt) / (per_vec * vcap)
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": total_bytes / kcnt,
                 "avg_launch_us": 1000.0 * kms / kcnt, "peak_source": peak_src,

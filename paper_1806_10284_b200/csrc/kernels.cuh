@@ -96,6 +96,7 @@ struct CGFuse {
     int max_iter;
     int nslab;                         // partial blocks per vector: [slab][vec][nb] (slab decomposition), 1
     int use_cond;                      // 1: set the CG graph's while-condition
+    int alpha_fold;                    // 1: k_zadj2 forms alpha itself from the (p, M p) partials (no cg_alpha kernel)
     cudaGraphConditionalHandle cond;
 };
 

@@ -405,6 +405,7 @@ struct bnf_solver {
     void* tm_base = nullptr;
     long long tm_planes = 0;
     bool use_z3 = false;      // persistent TMA-pipelined adjoint z pass (zpipe.cu)
+    bool alpha_fold_ok = true;   // CG alpha formed inside k_zadj2 (BNF_NO_ALPHA_FOLD=1: separate cg_alpha kernel)
     alignas(64) CUtensorMap tm_zu;        // TMA map of U for k_zadj3, valid for (tm_zu_base, tm_zu_slabs)
     void* tm_zu_base = nullptr;
     long long tm_zu_slabs = 0;
@@ -857,11 +858,11 @@ cudaError_t cg_iter_kernels(bnf_solver* s, const CGFuse& cg, double2* R, double2
     else BNF_K(launch_zfwd_cg(s->args, R, P, U, nvec, cg, st));
     if (s->use_plane) {
         BNF_K(run_plane(s, s->args, U, 3 * nvec, &cg, st));
-        BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        if (!cg.alpha_fold) BNF_K(launch_cg_finish(cg, 0, nvec, st));
     } else {
         BNF_K(launch_ypass(s->args, U, nvec, 0, st));
         BNF_K(launch_xpass_cg(s->args, U, nvec, cg, st));
-        BNF_K(launch_cg_finish(cg, 0, nvec, st));
+        if (!cg.alpha_fold) BNF_K(launch_cg_finish(cg, 0, nvec, st));
         BNF_K(launch_ypass(s->args, U, nvec, 1, st));
     }
     if (s->use_z2) BNF_K(run_zadj(s, U, R, nvec, 1, &cg, st));
@@ -959,6 +960,9 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
     // the partials (no per-CTA fences or last-CTA election; an election measured no faster)
     cg.nb_x = s->d_iter + 4;
     cg.nb_z = s->d_iter + 5;
+    // alpha formed inside k_zadj2 (one slab, no pipelined zadj3, not disabled by BNF_NO_ALPHA_FOLD):
+    // one kernel fewer per CG iteration
+    cg.alpha_fold = (s->use_z2 && !s->use_z3 && s->nsl == 1 && !s->dist && s->alpha_fold_ok) ? 1 : 0;
     int it = 0;
     if (!s->prof.on && s->use_graph) {
         cg.iter = s->d_iter;   // [3] counts the applications to still-active vectors on the device
@@ -984,11 +988,11 @@ int cg_solve_fused(bnf_solver* s, const double2* C, double2* X, int nvec, int* i
             else RUN("zfwd_cg", launch_zfwd_cg(s->args, R, P, U, nvec, cg, s->st));
             if (s->use_plane) {
                 RUN(plane_name(s->args, true), run_plane(s, s->args, U, 3 * nvec, &cg, s->st));
-                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
+                if (!cg.alpha_fold) RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
             } else {
                 RUN("yfwd", launch_ypass(s->args, U, nvec, 0, s->st));
                 RUN("xpass_cg", launch_xpass_cg(s->args, U, nvec, cg, s->st));
-                RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
+                if (!cg.alpha_fold) RUN("cg_alpha", launch_cg_finish(cg, 0, nvec, s->st));
                 RUN("yadj", launch_ypass(s->args, U, nvec, 1, s->st));
             }
             if (s->use_z2) RUN(zadj_name(s, true), run_zadj(s, U, R, nvec, 1, &cg, s->st));
@@ -1721,6 +1725,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     }
     s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
     s->args.plane_split = std::getenv("BNF_PLANE_SPLIT") ? std::atoi(std::getenv("BNF_PLANE_SPLIT")) : 1;
+    s->alpha_fold_ok = std::getenv("BNF_NO_ALPHA_FOLD") == nullptr;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

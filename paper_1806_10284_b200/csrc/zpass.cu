@@ -280,9 +280,37 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         cs[tid].cm = modes::col(p, i, j);
         cs[tid].base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
     }
-    const double alpha = MODE == 1 ? cg.alpha[vec] : 0.0;
+    double alpha = 0.0;
+    if (MODE == 1) {
+        if (SL == 0 && cg.alpha_fold) {
+            // alpha = (r, r) / (p, M p) from the plane pass's partials, formed by every CTA in the same
+            // fixed order (warp 0: lane-strided sums, then a xor butterfly), so all CTAs agree bit for bit;
+            // CTA (0, 0, vec) publishes it for the next zfwd2 (x update) and k_cg_xfinal
+            if (tid < 32) {
+                const int nbx = *cg.nb_x;
+                const double* pp = cg.part_x + (size_t)vec * nbx;
+                double acc = 0.0;
+                for (int t = tid; t < nbx; t += 32) acc += __ldcg(pp + t);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (tid == 0) {
+                    const double al = (cg.active[vec] && acc > 0.0) ? cg.rr[vec] / acc : 0.0;
+                    red[0] = make_double2(al, acc);
+                }
+            }
+        } else {
+            alpha = cg.alpha[vec];
+        }
+    }
     cp_async_wait0();
     __syncthreads();
+    if (MODE == 1 && SL == 0 && cg.alpha_fold) {
+        alpha = red[0].x;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+            cg.pmp[vec] = red[0].y;
+            cg.alpha[vec] = alpha;
+        }
+    }
     const int w = tid % W;
     const ColS& c = cs[w];
     const size_t gcol = col0 + w;
