@@ -242,12 +242,23 @@ __device__ __forceinline__ double2 root_tw(const double2* __restrict__ root, int
 // sit in one warp read consecutive entries (one wavefront per load).
 // Natural layout -> stage-2 layout.  On exit v[u*N2 + k2] = X[k1 + N1*k2]
 // with k1 = t + N2*u.  Two __syncthreads (buffer free on exit).
-template <int N1, int N2, int S, class X>
+// RS = true: `root` is a shared-memory copy of the table (plain loads instead of __ldg).
+template <int S, bool RS>
+__device__ __forceinline__ double2 root_at(const double2* __restrict__ root, int t) {
+    if constexpr (RS) {
+        const double2 w = root[t];
+        return S > 0 ? w : cconj(w);
+    } else {
+        return root_tw<S>(root, t);
+    }
+}
+
+template <int N1, int N2, int S, class X, bool RS = false>
 __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
     DFT<N1, S>::run(v);
     if (t > 0) {
 #pragma unroll
-        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, k1 * N2 + t));
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_at<S, RS>(root, k1 * N2 + t));
     }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) xch[X::idx(k1, t, w)] = v[k1];
@@ -267,7 +278,7 @@ __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2*
 }
 
 // Stage-2 layout -> natural layout (the same DFT run in reverse order).
-template <int N1, int N2, int S, class X>
+template <int N1, int N2, int S, class X, bool RS = false>
 __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
     constexpr int U = N1 / N2;
 #pragma unroll
@@ -286,9 +297,102 @@ __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, doubl
     __syncthreads();
     if (t > 0) {
 #pragma unroll
-        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_tw<S>(root, k1 * N2 + t));
+        for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_at<S, RS>(root, k1 * N2 + t));
     }
     DFT<N1, S>::run(v);
+}
+
+// ------------------------------------- 2N-point DFT as even / odd N-point halves
+// A sequence of 2N = 2 N1 N2 points held as pairs: thread t has x[2(N2 m + t)]
+// in a[m] and x[2(N2 m + t) + 1] in b[m] (m < N1, so every thread's elements are
+// adjacent pairs -- one 256-bit global access each).  N1 == N2 (one stage-2 DFT
+// per thread).  Forward (S): X[k] = E[k] + w_2N^{S k} O[k], X[k + N] = E[k] - ...,
+// E, O the N-point DFTs of the halves (one shared exchange round for both,
+// buffers xa and xb); on exit v[q] = X[t + N2 q], q < 2 N1.  `root` is the 2N
+// axis' [k1][t] stage table (entry k N2 + t = w_2N^{t k}): the N-point stage
+// roots are its even rows, w_2N^{t} is row 1.  RS: `root` in shared memory.
+template <int N1, int S, int K>
+__device__ __forceinline__ void eo_comb_fwd(const double2* a, const double2* b, double2* v, double2 wt) {
+    if constexpr (K < N1) {
+        const double2 o = cmul(twc<2 * N1, S, K>(b[K]), wt);
+        v[K] = cadd(a[K], o);
+        v[K + N1] = csub(a[K], o);
+        eo_comb_fwd<N1, S, K + 1>(a, b, v, wt);
+    }
+}
+template <int N1, int S, int K>
+__device__ __forceinline__ void eo_comb_inv(const double2* v, double2* a, double2* b, double2 wt) {
+    if constexpr (K < N1) {
+        a[K] = cadd(v[K], v[K + N1]);
+        b[K] = cmul(twc<2 * N1, S, K>(csub(v[K], v[K + N1])), wt);
+        eo_comb_inv<N1, S, K + 1>(v, a, b, wt);
+    }
+}
+
+template <int N1, int N2, int S, class X, bool RS>
+__device__ __forceinline__ void fft_fwd_eo(double2 (&a)[N1], double2 (&b)[N1], double2 (&v)[2 * N1], int t, int w,
+                                           double2* xa, double2* xb, const double2* root) {
+    static_assert(N1 == N2, "fft_fwd_eo: N1 == N2");
+    DFT<N1, S>::run(a);
+    DFT<N1, S>::run(b);
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) {
+            const double2 r = root_at<S, RS>(root, 2 * k1 * N2 + t);
+            a[k1] = cmul(a[k1], r);
+            b[k1] = cmul(b[k1], r);
+        }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) {
+        xa[X::idx(k1, t, w)] = a[k1];
+        xb[X::idx(k1, t, w)] = b[k1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int tt = 0; tt < N2; ++tt) {
+        a[tt] = xa[X::idx(t, tt, w)];
+        b[tt] = xb[X::idx(t, tt, w)];
+    }
+    __syncthreads();
+    DFT<N2, S>::run(a);
+    DFT<N2, S>::run(b);
+    const double2 wt = root_at<S, RS>(root, N2 + t);   // w_2N^{S t}
+    eo_comb_fwd<N1, S, 0>(a, b, v, wt);   // k = t + N2 k2 < N:  w_2N^{S k} = w_2N^{S t} w_{2N1}^{S k2}
+}
+
+// Inverse of the layout above (any sign S): v[q] = Y[t + N2 q] in, the 2N-point
+// DFT (sign S) out as pairs: a[m] = y[2(N2 m + t)], b[m] = y[2(N2 m + t) + 1].
+template <int N1, int N2, int S, class X, bool RS>
+__device__ __forceinline__ void fft_mirror_eo(double2 (&v)[2 * N1], double2 (&a)[N1], double2 (&b)[N1], int t, int w,
+                                              double2* xa, double2* xb, const double2* root) {
+    static_assert(N1 == N2, "fft_mirror_eo: N1 == N2");
+    const double2 wt = root_at<S, RS>(root, N2 + t);
+    eo_comb_inv<N1, S, 0>(v, a, b, wt);   // even outputs from Y[k] + Y[k+N], odd from (Y[k] - Y[k+N]) w^{S k}
+    DFT<N2, S>::run(a);
+    DFT<N2, S>::run(b);
+#pragma unroll
+    for (int tt = 0; tt < N2; ++tt) {
+        xa[X::idx(t, tt, w)] = a[tt];
+        xb[X::idx(t, tt, w)] = b[tt];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) {
+        a[k1] = xa[X::idx(k1, t, w)];
+        b[k1] = xb[X::idx(k1, t, w)];
+    }
+    __syncthreads();
+    if (t > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) {
+            const double2 r = root_at<S, RS>(root, 2 * k1 * N2 + t);
+            a[k1] = cmul(a[k1], r);
+            b[k1] = cmul(b[k1], r);
+        }
+    }
+    DFT<N1, S>::run(a);
+    DFT<N1, S>::run(b);
 }
 
 // ------------------------------------------ warp-local variants (no CTA barrier)

@@ -72,6 +72,8 @@ struct OpArgs {
                                 // (default on), bit 3 = CG x of zfwd prefetched into registers (measured slower)
     int plane_t;                // plane pass staged by TMA (plane_tma.cu)
     int plane_split;            // L2 plane pass: 2 = a cluster of two CTAs per plane (every other strip each)
+    int plane_rs;               // L2 plane pass: stage-root tables in shared memory (1)
+    int plane_xeo;              // L2 plane pass (128 plan): phase X as even / odd halves with 256-bit accesses (1)
 };
 
 struct Profiler;  // host-side, see solver.cu

@@ -63,6 +63,19 @@ __device__ __forceinline__ void st_hint(double2* ptr, double2 v, unsigned long l
                  : "memory");
 }
 
+// 256-bit global accesses (sm_100: one LDG/STG.E.ENL2.256 per adjacent complex pair)
+__device__ __forceinline__ void ld_pair(const double2* p, double2& a, double2& b) {
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void st_pair(double2* p, double2 a, double2 b) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+__device__ __forceinline__ void st_pair_hint(double2* p, double2 a, double2 b, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x),
+                 "d"(b.y), "l"(pol)
+                 : "memory");
+}
+
 template <int P>
 struct Cluster {
     __device__ static unsigned rank() { return P == 1 ? 0u : cgx::this_cluster().block_rank(); }
@@ -281,7 +294,13 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 // every phase (the phases meet at a cluster barrier, whose release / acquire
 // orders the strips written through L2): twice the CTAs, half the work each,
 // so the last wave of the launch is half as long.
-template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1>
+// RS = 1: the y / x stage-root tables are copied to shared memory once per CTA
+// (the 15 root loads per thread and FFT then leave the LSU global queue).
+// XEO = 1 (N = 128 plan only): phase X transforms each row as its even / odd
+// 64-point halves (fastfft fft_fwd_eo / fft_mirror_eo), so every thread holds
+// adjacent pairs and the row strips move with 256-bit loads and stores
+// (half the LSU global instructions of phase X).
+template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1, int RS = 0, int XEO = 0>
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
@@ -303,6 +322,17 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     unsigned char* eps_s = reinterpret_cast<unsigned char*>(D + C::SMEM);   // [N][N] material indices
     double* lut_s = reinterpret_cast<double*>(eps_s + (EPF ? N * N : 0));
     const bool epf = EPF && a.eps_idx != nullptr;
+    double2* ry_s = reinterpret_cast<double2*>(lut_s + 256);   // RS: stage roots [N1 N2] (y), then (x)
+    double2* rx_s = ry_s + N1 * N2;
+    if constexpr (RS) {
+        for (int q = tid; q < N1 * N2; q += C::NT) {
+            ry_s[q] = __ldg(a.py.root2 + q);
+            rx_s[q] = __ldg(a.px.root2 + q);
+        }
+        __syncthreads();
+    }
+    const double2* ry = RS ? ry_s : a.py.root2;
+    const double2* rx = RS ? rx_s : a.px.root2;
     if (epf) {
         for (int q = tid; q < 256; q += C::NT) lut_s[q] = __ldg(a.eps_lut + q);
         const unsigned char* src = a.eps_idx + (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * N * c;
@@ -322,7 +352,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
-        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
+        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>, RS != 0>(v, t, w, D, ry);
         const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
         const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
         const double2 wk = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N1 * M) % n12) * s3));
@@ -347,10 +377,39 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
     for (int r = r0; r < P; r += SPLIT) {
         const int b = r * CW + rw;
         double2* row = rowp(b);
+        const size_t rowofs = (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * ((size_t)b + (size_t)N * c);
+        if constexpr (XEO) {
+            static_assert(N1 == 2 * N2, "XEO: N1 = 2 N2");
+            using XH = fast::XchT<N2, N2, CW>;
+            double2 ea[N2], ob[N2];
+#pragma unroll
+            for (int m = 0; m < N2; ++m) ld_pair(row + 2 * (N2 * m + tx), ea[m], ob[m]);
+            fast::fft_fwd_eo<N2, N2, 1, XH, RS != 0>(ea, ob, v, tx, rw, D, D + XH::size, rx);
+            auto scale_eo = [&](auto eps_at) {
+#pragma unroll
+                for (int q = 0; q < N1; ++q) {
+                    const int aa = tx + N2 * q;
+                    const double s_ = a.inv_n * eps_at(aa);
+                    const double2 x = v[q];
+                    if (CG) pmp += s_ * (x.x * x.x + x.y * x.y);
+                    v[q] = cscale(x, s_);
+                }
+            };
+            if (epf) scale_eo([&](int aa) { return lut_s[eps_s[b * N + aa]]; });
+            else if (a.eps_idx) scale_eo([&](int aa) { return __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa)); });
+            else scale_eo([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
+            fast::fft_mirror_eo<N2, N2, -1, XH, RS != 0>(v, ea, ob, tx, rw, D, D + XH::size, rx);
+            if (a.plane_hint) {
+#pragma unroll
+                for (int m = 0; m < N2; ++m) st_pair_hint(row + 2 * (N2 * m + tx), ea[m], ob[m], pol_keep);
+            } else {
+#pragma unroll
+                for (int m = 0; m < N2; ++m) st_pair(row + 2 * (N2 * m + tx), ea[m], ob[m]);
+            }
+        } else {
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + tx];
-        fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
-        const size_t rowofs = (size_t)l * (SL ? a.nloc : p.n) + (size_t)N * ((size_t)b + (size_t)N * c);
+        fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>, RS != 0>(v, tx, rw, D, rx);
         // 1/(n eps) scaling (+ CG partial); the ε source is chosen once per strip, not per element
         auto scale = [&](auto eps_at) {
 #pragma unroll
@@ -367,13 +426,14 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         if (epf) scale([&](int aa) { return lut_s[eps_s[b * N + aa]]; });
         else if (a.eps_idx) scale([&](int aa) { return __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa)); });
         else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
-        fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>>(v, tx, rw, D, a.px.root2);
+        fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>, RS != 0>(v, tx, rw, D, rx);
         if (a.plane_hint) {
 #pragma unroll
             for (int m = 0; m < N1; ++m) st_hint(row + N2 * m + tx, v[m], pol_keep);
         } else {
 #pragma unroll
             for (int m = 0; m < N1; ++m) row[N2 * m + tx] = v[m];
+        }
         }
     }
     if constexpr (SPLIT == 1) __syncthreads();
@@ -387,7 +447,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
         const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
         fast::twiddle_natural<N1, N2>(v, wt, wu);
-        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>>(v, t, w, D, a.py.root2);
+        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, CW>, RS != 0>(v, t, w, D, ry);
         if (a.plane_hint) {
 #pragma unroll
             for (int u = 0; u < N1 / N2; ++u)
@@ -577,7 +637,8 @@ template <int N1, int N2, int P>
 cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFuse* cg, cudaStream_t st) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr bool EPF = (C::N % 16) == 0 && C::N <= 128;
-    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (EPF ? (size_t)C::N * C::N : 0) + 256 * sizeof(double);
+    const size_t smem = (size_t)C::SMEM * sizeof(double2) + (EPF ? (size_t)C::N * C::N : 0) + 256 * sizeof(double) +
+                        (a.plane_rs ? (size_t)2 * N1 * N2 * sizeof(double2) : 0);
     const dim3 g((unsigned)a.n3loc, (unsigned)nslab);
     auto run = [&](auto kern, auto cgarg) -> cudaError_t {
         cudaError_t e = allow_smem((const void*)kern, smem);
@@ -607,8 +668,26 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
             if (e != cudaSuccess) return e;
             return cudaLaunchKernelEx(&cfg, kern, U, a, cgarg);
         };
+        if (a.plane_rs) {
+            if (cg) return run2(k_plane_l2<N1, N2, P, 1, 0, 2, 1>, *cg);
+            return run2(k_plane_l2<N1, N2, P, 0, 0, 2, 1>, CGFuse{});
+        }
         if (cg) return run2(k_plane_l2<N1, N2, P, 1, 0, 2>, *cg);
         return run2(k_plane_l2<N1, N2, P, 0, 0, 2>, CGFuse{});
+    }
+    if constexpr (N1 == 2 * N2 && N1 * N2 == 128) {
+        if (a.plane_xeo) {
+            if (a.plane_rs) {
+                if (cg) return run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 1>, *cg);
+                return run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 1>, CGFuse{});
+            }
+            if (cg) return run(k_plane_l2<N1, N2, P, 1, 0, 1, 0, 1>, *cg);
+            return run(k_plane_l2<N1, N2, P, 0, 0, 1, 0, 1>, CGFuse{});
+        }
+    }
+    if (a.plane_rs) {
+        if (cg) return run(k_plane_l2<N1, N2, P, 1, 0, 1, 1>, *cg);
+        return run(k_plane_l2<N1, N2, P, 0, 0, 1, 1>, CGFuse{});
     }
     if (cg) return run(k_plane_l2<N1, N2, P, 1>, *cg);
     return run(k_plane_l2<N1, N2, P, 0>, CGFuse{});

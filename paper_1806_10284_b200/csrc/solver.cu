@@ -1726,6 +1726,8 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
     s->args.plane_split = std::getenv("BNF_PLANE_SPLIT") ? std::atoi(std::getenv("BNF_PLANE_SPLIT")) : 1;
     s->alpha_fold_ok = std::getenv("BNF_NO_ALPHA_FOLD") == nullptr;
+    s->args.plane_rs = std::getenv("BNF_PLANE_RS") ? std::atoi(std::getenv("BNF_PLANE_RS")) : 0;
+    s->args.plane_xeo = std::getenv("BNF_PLANE_XEO") ? std::atoi(std::getenv("BNF_PLANE_XEO")) : 0;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

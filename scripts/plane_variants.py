@@ -24,7 +24,10 @@ VARIANTS = {"yxy": {"BNF_NO_PLANE": "1"}, "cluster": {"BNF_PLANE": "1"},
             "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1"}, "warp_smem": {"BNF_PLANE_W": "1"},
             "warp_shfl": {"BNF_PLANE_W": "2"}, "tma": {"BNF_PLANE_T": "1"}, "tma_shfl": {"BNF_PLANE_T": "2"},
             "tma_pair": {"BNF_PLANE_T": "3"},
-           "l2_split": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_SPLIT": "2"}}
+           "l2_split": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_SPLIT": "2"},
+           "l2_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_RS": "1"},
+           "l2_xeo": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1"},
+           "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"}}
 
 
 def main():
@@ -44,7 +47,8 @@ def main():
     c = torch.randn(args.b * 2 * n, dtype=torch.complex128, device="cuda", generator=g)
     ref = None
     for name in args.variants.split(","):
-        for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T", "BNF_PLANE_SPLIT"):
+        for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T", "BNF_PLANE_SPLIT",
+                  "BNF_PLANE_RS", "BNF_PLANE_XEO"):
             os.environ.pop(k, None)
         os.environ.update(VARIANTS[name])
         st = torch.cuda.Stream()
