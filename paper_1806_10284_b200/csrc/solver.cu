@@ -729,6 +729,9 @@ int autotune_plane(bnf_solver* s, int nvec) {
     int pick = v0;
     for (int variant = v0 + 1; variant < nvar_all; ++variant)
         if (best[variant] > 0.f && best[variant] < best[pick]) pick = variant;
+    // the TMA-staged variants move 1.75x the algorithmic DRAM bytes of the L2 plane pass (its strips
+    // re-read from HBM, profiles/r02s2_ncu.json): within 3 % of the L2 variant, keep the L2 one
+    if (pick >= 5 && pick <= 7 && best[2] > 0.f && best[pick] > 0.97f * best[2]) pick = 2;
     set(pick);
     s->matvecs = mv0;
     s->prof.on = prof;
@@ -1726,7 +1729,9 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.plane_hint = std::getenv("BNF_PLANE_HINT") ? std::atoi(std::getenv("BNF_PLANE_HINT")) : 1;
     s->args.plane_split = std::getenv("BNF_PLANE_SPLIT") ? std::atoi(std::getenv("BNF_PLANE_SPLIT")) : 1;
     s->alpha_fold_ok = std::getenv("BNF_NO_ALPHA_FOLD") == nullptr;
-    s->args.plane_rs = std::getenv("BNF_PLANE_RS") ? std::atoi(std::getenv("BNF_PLANE_RS")) : 0;
+    // stage roots of the L2 plane pass in shared memory: default on (128^3: 123.5 vs 131.1 us at b = 1,
+    // 228 vs 241 at b = 2, profiles/r02s2_plane_options.jsonl)
+    s->args.plane_rs = std::getenv("BNF_PLANE_RS") ? std::atoi(std::getenv("BNF_PLANE_RS")) : 1;
     s->args.plane_xeo = std::getenv("BNF_PLANE_XEO") ? std::atoi(std::getenv("BNF_PLANE_XEO")) : 0;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
