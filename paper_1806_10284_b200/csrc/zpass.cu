@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     constexpr int NT = C::NT, TE = C::TE;
     extern __shared__ double2 sm[];   // [NA][TE]: y1 y2 (+1) | r1 r2 p1 p2; Ct = [0..3)
     __shared__ ColS cs[W];
+    __shared__ double2 rz_s[N1 * N2], hz_s[N1 * N2];   // z stage roots and e^{i pi k / n3} (RSZ)
+    constexpr bool RSZ = true;
     const ModeP& p = a.mp;
     const long long n = a.nloc;                         // per-component stride on this slab
     const int n1 = p.n1;
@@ -135,6 +137,12 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         cs[tid].cm = modes::col(p, i, j);
         cs[tid].base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
     }
+    if (RSZ && !(a.zcfg & 256))
+        for (int q = tid; q < N1 * N2; q += NT) {
+            rz_s[q] = __ldg(a.pz.root2 + q);
+            hz_s[q] = __ldg(a.hroot_z + q);
+        }
+    const bool rsz = RSZ && !(a.zcfg & 256);
     const double alpha_prev = MODE ? cg.alpha[vec] : 0.0;
     const double beta = MODE ? cg.beta[vec] : 0.0;
     const int w = tid % W;
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             pg[0] = u1;
             pg[n] = u2;
         }
-        const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
+        const double2 l2 = modes::lam3(p, c.cm, rsz ? hz_s[k] : __ldg(a.hroot_z + k));
         Coef o;
         const long long idx = c.cm.idx0 + kglob * k;
         modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
@@ -225,7 +233,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
         __syncthreads();
-        fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
+        if (rsz) fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>, true>(v, t, w, ct, rz_s);
+        else fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
         const unsigned long long nn = (unsigned long long)p.n, N3 = c.base3;   // e^{2 pi i P / n}: global n
         const double2 wt = tw_at(a.tw, ((unsigned long long)t * N3) % nn);
         const double2 wu = tw_at(a.tw, ((unsigned long long)N2 * N3) % nn);
@@ -250,6 +259,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     extern __shared__ double2 sm[];   // [3][TE]: U0 U1 U2 (r is streamed, not staged)
     __shared__ ColS cs[W];
     __shared__ double2 red[32];
+    __shared__ double2 rz_s[N1 * N2], hz_s[N1 * N2];   // z stage roots and e^{i pi k / n3}
+    const bool rsz = !(a.zcfg & 256);
     const ModeP& p = a.mp;
     const long long n = a.nloc;
     const int n1 = p.n1;
@@ -280,6 +291,11 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         cs[tid].cm = modes::col(p, i, j);
         cs[tid].base3 = (unsigned long long)((p.cbp * (long long)i + (p.n - p.n1m3) * (long long)j) % p.n);
     }
+    if (rsz)
+        for (int q = tid; q < N1 * N2; q += NT) {
+            rz_s[q] = __ldg(a.pz.root2 + q);
+            hz_s[q] = __ldg(a.hroot_z + q);
+        }
     double alpha = 0.0;
     if (MODE == 1) {
         if (SL == 0 && cg.alpha_fold) {
@@ -334,7 +350,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         for (int m = 0; m < N1; ++m) v[m] = ct[(N2 * m + t) * W + w];
         fast::twiddle_natural<N1, N2>(v, wt, wu);
         __syncthreads();
-        fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
+        if (rsz) fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>, true>(v, t, w, ct, rz_s);
+        else fast::fft_fwd<N1, N2, -1, fast::XchW<N1, N2, W>>(v, t, w, ct, a.pz.root2);
 #pragma unroll
         for (int u = 0; u < N1 / N2; ++u)
 #pragma unroll
@@ -357,7 +374,7 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
     // stay in registers (indexing them by (e - tid) / NT put them on the stack)
     auto elem = [&](const int e, double2 r1, double2 r2) {
         const int k = e / W;
-        const double2 l2 = modes::lam3(p, c.cm, __ldg(a.hroot_z + k));
+        const double2 l2 = modes::lam3(p, c.cm, rsz ? hz_s[k] : __ldg(a.hroot_z + k));
         Coef o;
         const long long idx = c.cm.idx0 + kglob * k;
         modes::coef(p, c.cm.lam1, c.cm.lam2, l2, idx == p.gamma, MODE ? 1 : op, o);
