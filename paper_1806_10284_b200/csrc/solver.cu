@@ -1667,8 +1667,9 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     s->args.vsf = 2 * n;
     s->args.nblk = n;
     // z-pass variant (kernels.cuh): default = register prefetch of the CG residual in zadj2
-    // (128^3, b = 2: 143 vs 149 us; the other bits measured no faster, profiles/r02_*)
-    s->args.zcfg = std::getenv("BNF_ZCFG") ? std::atoi(std::getenv("BNF_ZCFG")) : 4;
+    // (128^3, b = 2: 143 vs 149 us, profiles/r02_*) + the CG x tile staged with r, p in zfwd2 (bit 0:
+    // 176 vs 182 us at b = 2 once the stage roots moved to shared memory, profiles/r02s2_plane_options.jsonl)
+    s->args.zcfg = std::getenv("BNF_ZCFG") ? std::atoi(std::getenv("BNF_ZCFG")) : 5;
     s->args.fast = (std::getenv("BNF_NO_FAST") == nullptr) ? 1 : 0;
     // tile widths: keep each kernel's shared memory <= ~100 KB
     const int budget = 100 * 1024;
