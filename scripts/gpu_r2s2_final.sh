@@ -1,10 +1,10 @@
-# round-2 (session 2) evidence at the bench defaults (block 1, guard 2, 2 solvers per GPU):
-# every -m gpu test, smoke, the bench line, an ncu launch list of one k-point solve and a
-# --set full capture of the three CG passes (b = 1)
-TAG=${1:-r02s2}
+# round-2 (session 2) evidence at the bench defaults (block 1, guard 2, 2 solvers per GPU), part 1:
+# bench line, smoke, ncu launch list of one k-point solve, --set full of the CG passes (b = 1),
+# then the -m gpu tests except the two forced-variant families (part 2: scripts/gpu_r2s2_final2.sh)
+TAG=${1:-r02s2f}
 python paper_1806_10284_b200/build.py > gpurun_out/build_$TAG.log 2>&1 || { tail -20 gpurun_out/build_$TAG.log; exit 1; }
 timeout 1200 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo bench rc=$?
-tail -1 gpurun_out/bench_$TAG.log | cut -c1-600
+tail -1 gpurun_out/bench_$TAG.log | cut -c1-400
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo smoke rc=$?
 CMD="python bench.py --steps 1 --warmup 0 --per-gpu 1 --no-e2e --no-cpu"
 MIDDLE=$(python -c "import json; print(json.loads(open('gpurun_out/bench_$TAG.log').read().strip().splitlines()[-1])['middle'])")
@@ -16,10 +16,10 @@ case "$MIDDLE" in
   *) ;;
 esac
 echo middle=$MIDDLE
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 24000 --csv \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 24000 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu launches rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_(zfwd2|zadj2|plane)" -s 3000 -c 3 -o gpurun_out/full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu full rc=$?
 unset BNF_PLANE BNF_PLANE_L2 BNF_PLANE_SPLIT BNF_PLANE_T
-timeout 3300 python -m pytest tests -m gpu -q > gpurun_out/pytest_$TAG.log 2>&1; echo pytest rc=$?
-tail -5 gpurun_out/pytest_$TAG.log
+timeout 2400 python -m pytest tests -m gpu -q --durations=25 -k "not test_forced_middle_vs_oracle_full_size and not test_cg_fused_iterations_elementwise" > gpurun_out/pytest1_$TAG.log 2>&1; echo pytest1 rc=$?
+tail -32 gpurun_out/pytest1_$TAG.log
