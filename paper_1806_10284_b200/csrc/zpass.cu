@@ -296,42 +296,36 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
             rz_s[q] = __ldg(a.pz.root2 + q);
             hz_s[q] = __ldg(a.hroot_z + q);
         }
-    // alpha = (r, r) / (p, M p) from the middle's partials (alpha fold): every CTA sums them in the same
-    // fixed order (warp 0: lane-strided sums, then a xor butterfly), so all CTAs agree bit for bit, and
-    // CTA (0, 0, vec) publishes it for the next zfwd2 (x update) and k_cg_xfinal.  The partials are
-    // copied to shared memory with the U tile (cp.async) and summed after the tile barrier; alpha is
-    // first needed in phase A, behind the FFT's barriers.
-    __shared__ double2 pfx[1024];
-    const bool fold = MODE == 1 && SL == 0 && cg.alpha_fold;
-    int nbx = 0;
-    bool pf = false;
     double alpha = 0.0;
-    if (fold) {
-        nbx = *cg.nb_x;
-        pf = nbx <= 2048 && (nbx & 1) == 0;
-        const double* pp = cg.part_x + (size_t)vec * nbx;
-        if (pf) {
-            for (int q = tid; q < nbx / 2; q += NT) cp_async16(pfx + q, pp + 2 * q);
-            cp_async_commit();
-        } else if (tid < 32) {
-            double acc = 0.0;
-            for (int t = tid; t < nbx; t += 32) acc += __ldcg(pp + t);
+    if (MODE == 1) {
+        if (SL == 0 && cg.alpha_fold) {
+            // alpha = (r, r) / (p, M p) from the plane pass's partials, formed by every CTA in the same
+            // fixed order (warp 0: lane-strided sums, then a xor butterfly), so all CTAs agree bit for bit;
+            // CTA (0, 0, vec) publishes it for the next zfwd2 (x update) and k_cg_xfinal
+            if (tid < 32) {
+                const int nbx = *cg.nb_x;
+                const double* pp = cg.part_x + (size_t)vec * nbx;
+                double acc = 0.0;
+                for (int t = tid; t < nbx; t += 32) acc += __ldcg(pp + t);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (tid == 0) red[0] = make_double2((cg.active[vec] && acc > 0.0) ? cg.rr[vec] / acc : 0.0, acc);
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (tid == 0) {
+                    const double al = (cg.active[vec] && acc > 0.0) ? cg.rr[vec] / acc : 0.0;
+                    red[0] = make_double2(al, acc);
+                }
+            }
+        } else {
+            alpha = cg.alpha[vec];
         }
-    } else if (MODE == 1) {
-        alpha = cg.alpha[vec];
     }
     cp_async_wait0();
     __syncthreads();
-    if (fold && pf && tid < 32) {
-        const double* ps = reinterpret_cast<const double*>(pfx);
-        double acc = 0.0;
-        for (int t = tid; t < nbx; t += 32) acc += ps[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (tid == 0) red[0] = make_double2((cg.active[vec] && acc > 0.0) ? cg.rr[vec] / acc : 0.0, acc);
+    if (MODE == 1 && SL == 0 && cg.alpha_fold) {
+        alpha = red[0].x;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+            cg.pmp[vec] = red[0].y;
+            cg.alpha[vec] = alpha;
+        }
     }
     const int w = tid % W;
     const ColS& c = cs[w];
@@ -374,13 +368,6 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
         }
     }
     __syncthreads();
-    if (fold) {   // written by warp 0 before the FFT phase's barriers
-        alpha = red[0].x;
-        if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
-            cg.pmp[vec] = red[0].y;
-            cg.alpha[vec] = alpha;
-        }
-    }
     // ---- phase A: Pi^* combine, Sigma_op (+ CG residual update) ----
     double rr = 0.0;
     // RST 2: the element loop is unrolled over jj with a compile-time trip count so that rb1 / rb2

@@ -819,7 +819,9 @@ def test_zadj3_equals_zadj2(bnf, monkeypatch, idx, kidx, zcfg):
     from oracle import eigsolve
     cfg, n, kap = _cfg_case(idx, None, kidx)
     res = {}
-    for name, envs in (("z3", {"BNF_ZCFG": str(zcfg), "BNF_Z3": "1"}), ("z2", {"BNF_ZCFG": str(zcfg)})):
+    # k_zadj3 takes alpha from the separate cg_alpha kernel: compare with k_zadj2 doing the same
+    for name, envs in (("z3", {"BNF_ZCFG": str(zcfg), "BNF_Z3": "1"}),
+                       ("z2", {"BNF_ZCFG": str(zcfg), "BNF_NO_ALPHA_FOLD": "1"})):
         L, O, eps, S = _forced_solver(bnf, monkeypatch, envs, cfg, n)
         S.set_kappa(kap)
         c = vectors.complex_normal((2, 2 * O.nn), seed=5 + idx)
