@@ -69,11 +69,14 @@ struct OpArgs {
     long long nblk;             // n1 n2loc n3loc: one (slab pair, vector, component) exchange block
     int zcfg;                   // z-pass variant: bit 0 = stage x / r tiles with the inputs (CG), bit 1 = half-width
                                 // tiles, bit 2 = CG residual of zadj prefetched into registers before the mode loop
-                                // (default on), bit 3 = CG x of zfwd prefetched into registers (measured slower)
+                                // (default on), bit 3 = CG x of zfwd prefetched into registers (measured slower);
+                                // register budgets (128 plan): bit 9 = zadj2 CG for 4 CTAs/SM, bit 10 = zfwd2 CG
+                                // (x staged) for 2 CTAs/SM, bit 11 = zadj2 CG for 2 CTAs/SM (no spills)
     int plane_t;                // plane pass staged by TMA (plane_tma.cu)
     int plane_split;            // L2 plane pass: 2 = a cluster of two CTAs per plane (every other strip each)
     int plane_rs;               // L2 plane pass: stage-root tables in shared memory (1)
     int plane_xeo;              // L2 plane pass (128 plan): phase X as even / odd halves with 256-bit accesses (1)
+    int plane_ld;               // L2 plane pass (128 plan) load policy bits: 1 phase Y nc + L1::no_allocate, 2 phases X / Y* ld.cg
 };
 
 struct Profiler;  // host-side, see solver.cu

@@ -71,7 +71,9 @@ void herm_eig(int n, std::vector<cd>& A, std::vector<double>& w, std::vector<cd>
         e[j] = ac;
         D[j + 1] = (ac > 0.0) ? D[j] * (c / ac) : D[j];
     }
-    // Implicit QL (Wilkinson shift) with accumulation of rotations in Z.
+    // Implicit QL (Wilkinson shift) with accumulation of rotations in Z.  The loop
+    // structure (tst1 test, c2/c3/s2, el1/dl1) follows the public-domain EISPACK
+    // tql2 routine (Bowdler, Martin, Reinsch, Wilkinson; as in JAMA's tql2).
     std::vector<double> Z;
     if (want) {
         Z.assign((size_t)n * n, 0.0);

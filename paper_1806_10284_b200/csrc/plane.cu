@@ -76,6 +76,25 @@ __device__ __forceinline__ void st_pair_hint(double2* p, double2 a, double2 b, u
                  : "memory");
 }
 
+// Load policies of the L2 plane pass (LD template bits): phase Y reads U once from
+// HBM (read-only in that phase: non-coherent path, no L1 allocation, 256 B L2
+// fetch); phases X / Y* read strips this CTA wrote through L2 (ld.cg: L2 only).
+__device__ __forceinline__ double2 ld_y_first(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+template <int LD>
+__device__ __forceinline__ double2 ld_strip_y(const double2* p) {
+    if constexpr (LD & 1) return ld_y_first(p);
+    else return *p;
+}
+template <int LD>
+__device__ __forceinline__ double2 ld_strip_l2(const double2* p) {
+    if constexpr (LD & 2) return __ldcg(p);
+    else return *p;
+}
+
 template <int P>
 struct Cluster {
     __device__ static unsigned rank() { return P == 1 ? 0u : cgx::this_cluster().block_rank(); }
@@ -300,7 +319,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
 // 64-point halves (fastfft fft_fwd_eo / fft_mirror_eo), so every thread holds
 // adjacent pairs and the row strips move with 256-bit loads and stores
 // (half the LSU global instructions of phase X).
-template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1, int RS = 0, int XEO = 0>
+template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1, int RS = 0, int XEO = 0, int LD = 0>
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
@@ -351,7 +370,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
+        for (int m = 0; m < N1; ++m) v[m] = ld_strip_y<LD>(rowp(N2 * m + t) + i);
         fast::fft_fwd<N1, N2, 1, fast::XchW<N1, N2, CW>, RS != 0>(v, t, w, D, ry);
         const double2 wt = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3));
         const double2 wu = conj2(tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3));
@@ -408,7 +427,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
             }
         } else {
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = row[N2 * m + tx];
+        for (int m = 0; m < N1; ++m) v[m] = ld_strip_l2<LD>(row + N2 * m + tx);
         fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>, RS != 0>(v, tx, rw, D, rx);
         // 1/(n eps) scaling (+ CG partial); the ε source is chosen once per strip, not per element
         auto scale = [&](auto eps_at) {
@@ -443,7 +462,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         const int i = r * CW + w;
         const unsigned M = ((unsigned)p.m1 * (unsigned)i) % n12;
 #pragma unroll
-        for (int m = 0; m < N1; ++m) v[m] = rowp(N2 * m + t)[i];
+        for (int m = 0; m < N1; ++m) v[m] = ld_strip_l2<LD>(rowp(N2 * m + t) + i);
         const double2 wt = tw_at(a.tw, (unsigned long long)(((unsigned)t * M) % n12) * s3);
         const double2 wu = tw_at(a.tw, (unsigned long long)(((unsigned)N2 * M) % n12) * s3);
         fast::twiddle_natural<N1, N2>(v, wt, wu);
@@ -683,6 +702,15 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
             }
             if (cg) return run(k_plane_l2<N1, N2, P, 1, 0, 1, 0, 1>, *cg);
             return run(k_plane_l2<N1, N2, P, 0, 0, 1, 0, 1>, CGFuse{});
+        }
+    }
+    if constexpr (N1 * N2 == 128) {
+        if (a.plane_rs && a.plane_ld) {   // load-policy variants (BNF_PLANE_LD)
+            switch (a.plane_ld) {
+                case 1: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 1>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 1>, CGFuse{});
+                case 2: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 2>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 2>, CGFuse{});
+                default: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 3>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 3>, CGFuse{});
+            }
         }
     }
     if (a.plane_rs) {

@@ -1734,6 +1734,7 @@ int bnf_solver_create(const bnf_lattice* lat, const bnf_opts* opts, bnf_solver**
     // 228 vs 241 at b = 2, profiles/r02s2_plane_options.jsonl)
     s->args.plane_rs = std::getenv("BNF_PLANE_RS") ? std::atoi(std::getenv("BNF_PLANE_RS")) : 1;
     s->args.plane_xeo = std::getenv("BNF_PLANE_XEO") ? std::atoi(std::getenv("BNF_PLANE_XEO")) : 0;
+    s->args.plane_ld = std::getenv("BNF_PLANE_LD") ? std::atoi(std::getenv("BNF_PLANE_LD")) : 0;
     CK(s->phasebuf.ensure(16 * sizeof(unsigned long long)));
     CK(cudaMemset(s->phasebuf.p, 0, 16 * sizeof(unsigned long long)));
     s->args.prof = std::getenv("BNF_PHASE_PROF") ? s->phasebuf.as<unsigned long long>() : nullptr;

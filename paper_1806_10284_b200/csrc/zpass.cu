@@ -94,8 +94,8 @@ struct ColS {   // per-column constants shared through smem
 // CTAs per SM overlap one tile's loads with the other's FP64 work.  The
 // three component tiles of the FFT phase alias the consumed input stage.
 // MODE 0: U = Q_r Sigma_op Y (op = runtime 0 A_r / 1 M).  MODE 1: CG (op M).
-template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::NT))
+template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0, int MB = 0>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, MB ? MB : z_minb(ZCfg<N1, N2, W>::NT))
     k_zfwd2(const double2* __restrict__ Y, double2* __restrict__ U, OpArgs a, int op, double2* __restrict__ Pcg,
             double2* __restrict__ Xcg, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::N
 
 // ------------------------------------------------------------------ zadj
 // MODE 0: OUT = Sigma_op Q_r^* U.  MODE 1: CG, R -= alpha (Q_r^* U), (r, r) -> beta.
-template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0>
-__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, z_minb(ZCfg<N1, N2, W>::NT))
+template <int N1, int N2, int W, int MODE, int SL = 0, int RST = 0, int MB = 0>
+__global__ void __launch_bounds__(ZCfg<N1, N2, W>::NT, MB ? MB : z_minb(ZCfg<N1, N2, W>::NT))
     k_zadj2(const double2* __restrict__ U, double2* __restrict__ OUT, OpArgs a, int op, CGFuse cg) {
     using C = ZCfg<N1, N2, W>;
     constexpr int NT = C::NT, TE = C::TE;
@@ -474,6 +474,10 @@ static cudaError_t zfwd2_t(const OpArgs& a, const double2* Y, double2* U, int nv
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if constexpr (ZCfg<N1, N2, W>::NT <= 256) {   // zcfg bit 1024: x tile staged, compiled for 2 CTAs per SM
+        // (its 6-tile stage admits only 2 per SM anyway; the 3-CTA register cap made ptxas spill)
+        if (mode && rst == 1 && !sl && (a.zcfg & 1024)) return go(k_zfwd2<N1, N2, W, 1, 0, 1, 2>, 1, P, X, *cg);
+    }
     if (mode && rst == 2) return sl ? go(k_zfwd2<N1, N2, W, 1, 1, 2>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0, 2>, 1, P, X, *cg);
     if (mode && rst) return sl ? go(k_zfwd2<N1, N2, W, 1, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0, 1>, 1, P, X, *cg);
     if (mode) return sl ? go(k_zfwd2<N1, N2, W, 1, 1>, 1, P, X, *cg) : go(k_zfwd2<N1, N2, W, 1, 0>, 1, P, X, *cg);
@@ -496,6 +500,11 @@ static cudaError_t zadj2_t(const OpArgs& a, const double2* U, double2* OUT, int 
         return cudaGetLastError();
     };
     const bool sl = a.nslab > 1;
+    if constexpr (ZCfg<N1, N2, W>::NT <= 256) {   // zcfg bit 512: compiled for 4 resident CTAs per SM
+        if (mode && rst == 2 && !sl && (a.zcfg & 512)) return go(k_zadj2<N1, N2, W, 1, 0, 2, 4>, 1, *cg);
+        if (mode && rst == 2 && !sl && (a.zcfg & 2048)) return go(k_zadj2<N1, N2, W, 1, 0, 2, 2>, 1, *cg);
+        if (mode && rst == 1 && !sl && (a.zcfg & 2048)) return go(k_zadj2<N1, N2, W, 1, 0, 1, 2>, 1, *cg);
+    }
     if (mode && rst == 2) return sl ? go(k_zadj2<N1, N2, W, 1, 1, 2>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0, 2>, 1, *cg);
     if (mode && rst) return sl ? go(k_zadj2<N1, N2, W, 1, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0, 1>, 1, *cg);
     if (mode) return sl ? go(k_zadj2<N1, N2, W, 1, 1>, 1, *cg) : go(k_zadj2<N1, N2, W, 1, 0>, 1, *cg);

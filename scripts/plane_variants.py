@@ -27,7 +27,13 @@ VARIANTS = {"yxy": {"BNF_NO_PLANE": "1"}, "cluster": {"BNF_PLANE": "1"},
            "l2_split": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_SPLIT": "2"},
            "l2_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_RS": "1"},
            "l2_xeo": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1"},
-           "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"}}
+           "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"},
+           "l2_ld1": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "1"},
+           "l2_ld2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "2"},
+           "l2_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "3"}}
+# z-pass register-budget variants (BNF_ZCFG bits, kernels.cuh zcfg), with the L2 plane middle
+for _z in (5, 1029, 517, 2053, 2049, 3077, 3073):
+    VARIANTS["z%d" % _z] = {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_ZCFG": str(_z)}
 
 
 def main():
@@ -48,7 +54,7 @@ def main():
     ref = None
     for name in args.variants.split(","):
         for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T", "BNF_PLANE_SPLIT",
-                  "BNF_PLANE_RS", "BNF_PLANE_XEO"):
+                  "BNF_PLANE_RS", "BNF_PLANE_XEO", "BNF_PLANE_LD", "BNF_ZCFG"):
             os.environ.pop(k, None)
         os.environ.update(VARIANTS[name])
         st = torch.cuda.Stream()

@@ -498,15 +498,16 @@ MIDDLES = {"cluster": {"BNF_PLANE": "1"}, "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2
            "l2_split": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_SPLIT": "2"},
            "l2_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_RS": "1"},
            "l2_xeo": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1"},
-           "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"}}
+           "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"},
+           "l2_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "3"}}
 
 
-ONLY128 = ("l2_rs", "l2_xeo", "l2_xeo_rs")   # stage roots in smem / even-odd x phase: 128 plan only
+ONLY128 = ("l2_rs", "l2_xeo", "l2_xeo_rs", "l2_ld3")   # stage roots in smem / even-odd x phase: 128 plan only
 
 
 def _forced_solver(bnf, monkeypatch, envs, cfg, n, **kw):
     for k in ("BNF_PLANE", "BNF_PLANE_L2", "BNF_NO_PLANE", "BNF_PLANE_W", "BNF_PLANE_T", "BNF_PLANE_SPLIT",
-                  "BNF_PLANE_RS", "BNF_PLANE_XEO"):
+                  "BNF_PLANE_RS", "BNF_PLANE_XEO", "BNF_PLANE_LD"):
         monkeypatch.delenv(k, raising=False)
     for k, v in envs.items():
         monkeypatch.setenv(k, v)
@@ -574,11 +575,12 @@ def test_cg_fused_iterations_elementwise(bnf, monkeypatch, idx, kidx, middle):
 
 
 @pytest.mark.parametrize("idx,kidx", [(3, 5), (4, 12)], ids=["96", "128"])
-@pytest.mark.parametrize("zcfg", [0, 1, 2, 4, 6, 8, 12])
+@pytest.mark.parametrize("zcfg", [0, 1, 2, 4, 6, 8, 12, 517, 3077, 2049])
 def test_cg_fused_zpass_variants(bnf, monkeypatch, idx, kidx, zcfg):
     """Every z-pass tile / prefetch configuration (BNF_ZCFG bits: 1 staged
     r and x tiles, 2 narrow tiles, 4 residual prefetch in registers, 8 x
-    prefetch in registers) gives the same CG iterates as plain CG on the
+    prefetch in registers; 512 / 1024 / 2048 register budgets of the 128
+    plan's CG passes) gives the same CG iterates as plain CG on the
     oracle's M, x_3 to 1e-11 relative, b = 2."""
     cfg, n, kap = _cfg_case(idx, None, kidx)
     L, O, eps, S = _forced_solver(bnf, monkeypatch, {"BNF_ZCFG": str(zcfg)}, cfg, n)
