@@ -253,7 +253,16 @@ __device__ __forceinline__ double2 root_at(const double2* __restrict__ root, int
     }
 }
 
-template <int N1, int N2, int S, class X, bool RS = false>
+// WS = true: the N2 threads of a sequence sit in one warp and the warp's sequences own a private
+// region of `xch` (XchT with w = tid / N2, N2 | 32), so the exchange is ordered by __syncwarp and
+// the warps of the CTA run independently.
+template <bool WS>
+__device__ __forceinline__ void xch_sync() {
+    if constexpr (WS) __syncwarp();
+    else __syncthreads();
+}
+
+template <int N1, int N2, int S, class X, bool RS = false, bool WS = false>
 __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
     DFT<N1, S>::run(v);
     if (t > 0) {
@@ -262,7 +271,7 @@ __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2*
     }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) xch[X::idx(k1, t, w)] = v[k1];
-    __syncthreads();
+    xch_sync<WS>();
     constexpr int U = N1 / N2;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -274,11 +283,11 @@ __device__ __forceinline__ void fft_fwd(double2 (&v)[N1], int t, int w, double2*
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) v[u * N2 + k2] = a[k2];
     }
-    __syncthreads();
+    xch_sync<WS>();
 }
 
 // Stage-2 layout -> natural layout (the same DFT run in reverse order).
-template <int N1, int N2, int S, class X, bool RS = false>
+template <int N1, int N2, int S, class X, bool RS = false, bool WS = false>
 __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, double2* xch, const double2* root) {
     constexpr int U = N1 / N2;
 #pragma unroll
@@ -291,10 +300,10 @@ __device__ __forceinline__ void fft_mirror(double2 (&v)[N1], int t, int w, doubl
 #pragma unroll
         for (int tt = 0; tt < N2; ++tt) xch[X::idx(k1, tt, w)] = a[tt];
     }
-    __syncthreads();
+    xch_sync<WS>();
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) v[k1] = xch[X::idx(k1, t, w)];
-    __syncthreads();
+    xch_sync<WS>();
     if (t > 0) {
 #pragma unroll
         for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], root_at<S, RS>(root, k1 * N2 + t));

@@ -323,6 +323,10 @@ template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1, int RS = 0, 
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
+    // LD bit 4: phase X's FFT exchanges are warp-local (a row's N2 threads are consecutive lanes and
+    // XchT gives each row its own region), so they synchronise with __syncwarp and the CTA's warps
+    // drift apart inside the phase (loads of one warp overlap the FFT of another)
+    constexpr bool XW = (LD & 4) != 0 && (32 % N2) == 0 && XEO == 0;
     extern __shared__ double2 D[];
     const ModeP& p = a.mp;
     const int tid = threadIdx.x;
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         } else {
 #pragma unroll
         for (int m = 0; m < N1; ++m) v[m] = ld_strip_l2<LD>(row + N2 * m + tx);
-        fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>, RS != 0>(v, tx, rw, D, rx);
+        fast::fft_fwd<N1, N2, 1, fast::XchT<N1, N2, CW>, RS != 0, XW>(v, tx, rw, D, rx);
         // 1/(n eps) scaling (+ CG partial); the ε source is chosen once per strip, not per element
         auto scale = [&](auto eps_at) {
 #pragma unroll
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::
         if (epf) scale([&](int aa) { return lut_s[eps_s[b * N + aa]]; });
         else if (a.eps_idx) scale([&](int aa) { return __ldg(a.eps_lut + __ldg(a.eps_idx + rowofs + aa)); });
         else scale([&](int aa) { return __ldg(a.eps_inv + rowofs + aa); });
-        fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>, RS != 0>(v, tx, rw, D, rx);
+        fast::fft_mirror<N1, N2, -1, fast::XchT<N1, N2, CW>, RS != 0, XW>(v, tx, rw, D, rx);
         if (a.plane_hint) {
 #pragma unroll
             for (int m = 0; m < N1; ++m) st_hint(row + N2 * m + tx, v[m], pol_keep);
@@ -709,7 +713,10 @@ cudaError_t launch_plane_l2_t(const OpArgs& a, double2* U, int nslab, const CGFu
             switch (a.plane_ld) {
                 case 1: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 1>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 1>, CGFuse{});
                 case 2: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 2>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 2>, CGFuse{});
-                default: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 3>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 3>, CGFuse{});
+                case 3: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 3>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 3>, CGFuse{});
+                case 4: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 4>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 4>, CGFuse{});
+                case 6: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 6>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 6>, CGFuse{});
+                default: return cg ? run(k_plane_l2<N1, N2, P, 1, 0, 1, 1, 0, 7>, *cg) : run(k_plane_l2<N1, N2, P, 0, 0, 1, 1, 0, 7>, CGFuse{});
             }
         }
     }
