@@ -76,7 +76,7 @@ struct OpArgs {
     int plane_split;            // L2 plane pass: 2 = a cluster of two CTAs per plane (every other strip each)
     int plane_rs;               // L2 plane pass: stage-root tables in shared memory (1)
     int plane_xeo;              // L2 plane pass (128 plan): phase X as even / odd halves with 256-bit accesses (1)
-    int plane_ld;               // L2 plane pass (128 plan) load policy bits: 1 phase Y nc + L1::no_allocate, 2 phases X / Y* ld.cg
+    int plane_ld;               // L2 plane pass (128 plan) load policy bits: 1 phase Y nc + L1::no_allocate, 2 phases X / Y* ld.cg, 4 phase X exchanges by CTA barriers instead of __syncwarp
 };
 
 struct Profiler;  // host-side, see solver.cu

@@ -323,10 +323,11 @@ template <int N1, int N2, int P, int CG, int SL = 0, int SPLIT = 1, int RS = 0, 
 __global__ void __launch_bounds__(PlaneCfg<N1, N2, P>::NT, PlaneCfg<N1, N2, P>::NT <= 256 ? 2 : 1) k_plane_l2(double2* __restrict__ U, OpArgs a, CGFuse cgf) {
     using C = PlaneCfg<N1, N2, P>;
     constexpr int N = C::N, CW = C::CW;
-    // LD bit 4: phase X's FFT exchanges are warp-local (a row's N2 threads are consecutive lanes and
-    // XchT gives each row its own region), so they synchronise with __syncwarp and the CTA's warps
-    // drift apart inside the phase (loads of one warp overlap the FFT of another)
-    constexpr bool XW = (LD & 4) != 0 && (32 % N2) == 0 && XEO == 0;
+    // Phase X's FFT exchanges are warp-local (a row's N2 threads are consecutive lanes and XchT gives
+    // each row its own region), so they synchronise with __syncwarp and the CTA's warps drift apart
+    // inside the phase (the loads of one warp overlap the FFT of another).  LD bit 4 restores the
+    // CTA-wide barriers (A/B switch, 128 plan).
+    constexpr bool XW = (LD & 4) == 0 && (32 % N2) == 0 && (C::NT % 32) == 0 && XEO == 0;
     extern __shared__ double2 D[];
     const ModeP& p = a.mp;
     const int tid = threadIdx.x;

@@ -1,8 +1,7 @@
-# round-2 (session 2) evidence at the bench defaults (block 1, guard 2, 2 solvers per GPU), part 1:
+# round-2 (session 4) final evidence at the bench defaults (block 1, guard 2, 2 solvers per GPU):
 # bench line, smoke, ncu launch list of one k-point solve, --set full of the CG passes (b = 1),
-# then the -m gpu tests except the two forced-variant families (part 2: scripts/gpu_r2s2_final2.sh)
-TAG=${1:-r02s2f}
-python paper_1806_10284_b200/build.py > gpurun_out/build_$TAG.log 2>&1 || { tail -20 gpurun_out/build_$TAG.log; exit 1; }
+# then the whole -m gpu suite with durations
+TAG=${1:-r02s4f}
 timeout 1200 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo bench rc=$?
 tail -1 gpurun_out/bench_$TAG.log | cut -c1-400
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo smoke rc=$?
@@ -21,5 +20,3 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 24000 
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_(zfwd2|zadj2|plane)" -s 3000 -c 3 -o gpurun_out/full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu full rc=$?
 unset BNF_PLANE BNF_PLANE_L2 BNF_PLANE_SPLIT BNF_PLANE_T
-timeout 2400 python -m pytest tests -m gpu -q --durations=25 -k "not test_forced_middle_vs_oracle_full_size and not test_cg_fused_iterations_elementwise" > gpurun_out/pytest1_$TAG.log 2>&1; echo pytest1 rc=$?
-tail -32 gpurun_out/pytest1_$TAG.log

@@ -31,9 +31,9 @@ VARIANTS = {"yxy": {"BNF_NO_PLANE": "1"}, "cluster": {"BNF_PLANE": "1"},
            "l2_ld1": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "1"},
            "l2_ld2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "2"},
            "l2_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "3"},
-           "l2_xw": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "4"},
-           "l2_xw_ld2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "6"},
-           "l2_xw_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "7"}}
+           "l2_noxw": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "4"},
+           "l2_noxw_ld2": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "6"},
+           "l2_noxw_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "7"}}
 # z-pass register-budget variants (BNF_ZCFG bits, kernels.cuh zcfg), with the L2 plane middle
 for _z in (5, 1029, 517, 2053, 2049, 3077, 3073):
     VARIANTS["z%d" % _z] = {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_ZCFG": str(_z)}

@@ -500,11 +500,11 @@ MIDDLES = {"cluster": {"BNF_PLANE": "1"}, "l2": {"BNF_PLANE": "1", "BNF_PLANE_L2
            "l2_xeo": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1"},
            "l2_xeo_rs": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_XEO": "1", "BNF_PLANE_RS": "1"},
            "l2_ld3": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "3"},
-           "l2_xw": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "4"},
-           "l2_xw_ld": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "7"}}
+           "l2_noxw": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "4"},
+           "l2_noxw_ld": {"BNF_PLANE": "1", "BNF_PLANE_L2": "1", "BNF_PLANE_LD": "7"}}
 
 
-ONLY128 = ("l2_rs", "l2_xeo", "l2_xeo_rs", "l2_ld3", "l2_xw", "l2_xw_ld")   # stage roots in smem / even-odd x phase: 128 plan only
+ONLY128 = ("l2_rs", "l2_xeo", "l2_xeo_rs", "l2_ld3", "l2_noxw", "l2_noxw_ld")   # stage roots in smem / even-odd x phase: 128 plan only
 
 
 def _forced_solver(bnf, monkeypatch, envs, cfg, n, **kw):
