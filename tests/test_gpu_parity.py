@@ -24,6 +24,17 @@ from synthetic import configs, eps as E, vectors  # noqa: E402
 
 OP_TOL = 1e-12
 
+# The default -m gpu run is the CORE matrix (every autotune / production kernel at every BASELINE grid,
+# every opt-in variant at the bench grid); BNF_TEST_FULL=1 adds the exhaustive variant x grid products
+# (about an hour on one B200 with the oracle on the host cores; run per session, DESIGN 7b).
+FULL_MATRIX = os.environ.get("BNF_TEST_FULL", "") not in ("", "0")
+exhaustive = pytest.mark.skipif(not FULL_MATRIX, reason="exhaustive variant matrix: set BNF_TEST_FULL=1")
+
+
+def _case(*vals, core=True, id=None):
+    return pytest.param(*vals, marks=() if core else (exhaustive,), id=id)
+
+
 
 @pytest.fixture(scope="module")
 def bnf():
@@ -265,8 +276,9 @@ def _full_goldens():
     return sorted(f for f in os.listdir(gdir) if f.startswith("full_c") and f.endswith("_oracle.json"))
 
 
-@pytest.mark.parametrize("fname", _full_goldens())
-@pytest.mark.parametrize("block,guard", [(4, 4), (2, 2)], ids=["b4g4", "bench_b2g2"])
+@pytest.mark.parametrize("block,guard,fname", [
+    _case(b, g_, f, core=(b == 4 or f.startswith("full_c4")), id="%s-%s" % (tag, f))
+    for b, g_, tag in ((4, 4, "b4g4"), (2, 2, "bench_b2g2")) for f in _full_goldens()])
 def test_full_size_eigenvalues_vs_oracle(bnf, golden_dir, fname, block, guard):
     """BASELINE configs at their FULL grids (k-subsets incl. Gamma and, for
     config 4, the k-points the default bench times): the nev smallest
@@ -568,8 +580,13 @@ def _oracle_cg_cached(idx, kidx, seed, ks):
     return _ORACLE_CACHE[key]
 
 
-@pytest.mark.parametrize("idx,kidx", [(3, 5), (4, 7), (5, 0)], ids=["96", "128", "256"])
-@pytest.mark.parametrize("middle", list(MIDDLES))
+AUTOTUNE3 = ("cluster", "l2", "yxy")   # the three middles the round-1 autotune chose between
+
+
+@pytest.mark.parametrize("idx,kidx,middle", [
+    _case(idx, kidx, m, core=(m in AUTOTUNE3 or (idx == 4 and m != "l2_rs")), id="%s-%s" % (m, tag))
+    for idx, kidx, tag in ((3, 5, "96"), (4, 7, "128"), (5, 0, "256")) for m in MIDDLES
+    if idx == 4 or m not in ONLY128])
 def test_forced_middle_vs_oracle_full_size(bnf, monkeypatch, idx, kidx, middle):
     """Every real-space middle (cluster plane, L2 plane, y/x/y passes) forced
     at the full 96^3, 128^3 and 256^3 grids, b = 2 (the bench's launch):
@@ -590,8 +607,10 @@ def test_forced_middle_vs_oracle_full_size(bnf, monkeypatch, idx, kidx, middle):
     S.close()
 
 
-@pytest.mark.parametrize("idx,kidx", [(2, 9), (4, 12)], ids=["64", "128"])
-@pytest.mark.parametrize("middle", list(MIDDLES))
+@pytest.mark.parametrize("idx,kidx,middle", [
+    _case(idx, kidx, m, core=(m in AUTOTUNE3 or (idx == 4 and m in ("l2_split", "tma_shfl", "l2_noxw"))),
+          id="%s-%s" % (m, tag))
+    for idx, kidx, tag in ((2, 9, "64"), (4, 12, "128")) for m in MIDDLES if idx == 4 or m not in ONLY128])
 def test_cg_fused_iterations_elementwise(bnf, monkeypatch, idx, kidx, middle):
     """The CG-fused passes (zfwd2_cg: x += alpha_prev p, p <- r + beta p;
     middle_cg: (p, Mp) -> alpha; zadj2_cg: r -= alpha Mp, (r, r) -> beta)
@@ -616,8 +635,9 @@ def test_cg_fused_iterations_elementwise(bnf, monkeypatch, idx, kidx, middle):
     S.close()
 
 
-@pytest.mark.parametrize("idx,kidx", [(3, 5), (4, 12)], ids=["96", "128"])
-@pytest.mark.parametrize("zcfg", [0, 1, 2, 4, 6, 8, 12, 517, 3077, 2049])
+@pytest.mark.parametrize("idx,kidx,zcfg", [
+    _case(idx, kidx, z, core=(idx == 4), id="%d-%s" % (z, tag))
+    for idx, kidx, tag in ((3, 5, "96"), (4, 12, "128")) for z in (0, 1, 2, 4, 6, 8, 12, 517, 3077, 2049)])
 def test_cg_fused_zpass_variants(bnf, monkeypatch, idx, kidx, zcfg):
     """Every z-pass tile / prefetch configuration (BNF_ZCFG bits: 1 staged
     r and x tiles, 2 narrow tiles, 4 residual prefetch in registers, 8 x
@@ -711,7 +731,7 @@ def test_virtual_slabs_eigenvalues(bnf):
         assert r <= 1e-8
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [_case(2), _case(4, core=False)])
 def test_virtual_slabs_config5_golden(bnf, golden_dir, P):
     """Config 5 (FCC diamond 256^3, one k) on P virtual slabs: eigenvalues equal
     the oracle golden (tests/golden/full_c5_k0_oracle.json) to 1e-10."""
@@ -819,7 +839,7 @@ def test_relaxed_inner_tolerance_same_eigenvalues(bnf):
     assert st["matvecs"] < st0["matvecs"], (st["matvecs"], st0["matvecs"])
 
 
-@pytest.mark.parametrize("fname", ["full_c2_k9_oracle.json", "full_c4_k12_oracle.json"])
+@pytest.mark.parametrize("fname", [_case("full_c2_k9_oracle.json"), _case("full_c4_k12_oracle.json", core=False)])
 def test_lobpcg_matches_golden(bnf, golden_dir, fname):
     """NEXT-1 LOBPCG (bnf_opts.method = 1: A_r preconditioned by Sigma_r^{-2},
     no inner solves) returns the oracle golden eigenvalues to 1e-10 with every
@@ -848,8 +868,8 @@ def test_gyroid_bcc_vs_dense_oracle(bnf):
     np.testing.assert_allclose(lam, dense, rtol=1e-10)
 
 
-@pytest.mark.parametrize("idx,kidx", [(4, 12)], ids=["128"])
-@pytest.mark.parametrize("zcfg", [4, 36, 68])
+@pytest.mark.parametrize("idx,kidx,zcfg", [_case(4, 12, 4, id="4-128"), _case(4, 12, 36, core=False, id="36-128"),
+                                           _case(4, 12, 68, core=False, id="68-128")])
 def test_zadj3_equals_zadj2(bnf, monkeypatch, idx, kidx, zcfg):
     """The persistent pipelined adjoint z pass (zpipe.cu; opt-in
     BNF_Z3=1) does k_zadj2's arithmetic in the same order, partials included:
