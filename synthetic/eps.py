@@ -88,17 +88,32 @@ def _inside(X, shape, a_orig):
     return inside
 
 
-def _geometric(shape, a_snap, delta, n, a_orig, chunk=1 << 18, eps_in=EPS_IN):
+def _geometric(shape, a_snap, delta, n, a_orig, chunk=1 << 15, eps_in=EPS_IN):
+    """Chunks of Yee points are independent, so they run on a thread pool (numpy releases the GIL in the
+    distance kernels); every chunk computes exactly what the serial loop computed."""
+    import concurrent.futures
+    import os
     inv = np.linalg.inv(np.asarray(a_snap, dtype=np.float64))
+    a_o = np.asarray(a_orig, dtype=np.float64)
     out = []
+    workers = max(1, min(16, os.cpu_count() or 1))
     for comp in range(3):
         x = yee_points(delta, n, comp)
         e = np.empty(x.shape[0])
-        for s in range(0, x.shape[0], chunk):
+
+        def one(s, x=x, e=e):
             f = x[s:s + chunk] @ inv.T
             f -= np.floor(f)
-            X = f @ np.asarray(a_orig, dtype=np.float64).T
+            X = f @ a_o.T
             e[s:s + chunk] = np.where(_inside(X, shape, a_orig), eps_in, EPS_OUT)
+
+        starts = range(0, x.shape[0], chunk)
+        if workers > 1 and len(starts) > 1:
+            with concurrent.futures.ThreadPoolExecutor(workers) as ex:
+                list(ex.map(one, starts))
+        else:
+            for s in starts:
+                one(s)
         out.append(e.reshape(n[2], n[1], n[0]))
     return out
 

@@ -44,10 +44,22 @@ def bnf():
     return m
 
 
+_EPS_CACHE = {}
+
+
+def _eps_cached(shape, n, O):
+    """synthetic.eps.sample is a host-side geometry rasteriser (minutes at 256^3): one evaluation per
+    (lattice, grid, shape) per session, shared read-only by the tests."""
+    key = (shape, tuple(n), np.asarray(O.a).tobytes())
+    if key not in _EPS_CACHE:
+        _EPS_CACHE[key] = E.sample(shape, n, O.a, O.delta, O.a_canon)
+    return _EPS_CACHE[key]
+
+
 def _setup(bnf, a_raw, n, shape, **kw):
     L = bnf.Lattice(a_raw, n)
     O = olat.snap(a_raw, n)
-    eps = E.sample(shape, n, O.a, O.delta, O.a_canon)
+    eps = _eps_cached(shape, n, O)
     S = bnf.Solver(L, **kw)
     S.set_epsilon(E.stacked(eps))
     return L, O, eps, S
@@ -545,7 +557,7 @@ def _oracle_apply_cached(idx, kidx, seed, nvec, sample=None):
     if key not in _ORACLE_CACHE:
         cfg, n, kap = _cfg_case(idx, None, kidx)
         O = olat.snap(cfg.a_raw, n)
-        eps = E.sample(cfg.shape, n, O.a, O.delta, O.a_canon)
+        eps = _eps_cached(cfg.shape, n, O)
         op = fftop.NFSEPOperator(O, kap, eps)
         y = vectors.complex_normal((2, 2 * O.nn), seed=seed)
         sel = None if sample is None else np.random.default_rng(idx).choice(2 * O.nn, sample, replace=False)
@@ -566,7 +578,7 @@ def _oracle_cg_cached(idx, kidx, seed, ks):
         from oracle import eigsolve
         cfg, n, kap = _cfg_case(idx, None, kidx)
         O = olat.snap(cfg.a_raw, n)
-        eps = E.sample(cfg.shape, n, O.a, O.delta, O.a_canon)
+        eps = _eps_cached(cfg.shape, n, O)
         op = fftop.NFSEPOperator(O, kap, eps)
         c = vectors.complex_normal((2, 2 * O.nn), seed=seed)
         out = {}
